@@ -1,0 +1,166 @@
+/*
+ * pbvd.h -- C ABI of the B200 (sm_100a) parallel block-based Viterbi decoder.
+ *
+ * The operation is the PBVD of Peng et al., arXiv 1608.00066 ("P:n" = line n
+ * of PAPER.md):
+ *   - a received stream of soft values is cut into blocks of D decoded stages;
+ *     block b decodes [bD, bD+D) and runs its forward pass over the parallel
+ *     block [bD-L, bD+D+L) (truncated block M = L, decoding block D,
+ *     traceback block L);
+ *   - the forward pass is the add-compare-select recursion of Eq. 1
+ *     on the trellis of Eq. 2, with the branch metrics reduced to
+ *     the 2^R distinct codeword metrics per stage (Eqs. 3-6);
+ *   - one survivor bit per state per stage is kept ("bit 0 denotes the upper
+ *     branch, bit 1 the lower");
+ *   - the traceback (Alg. 1 K2) starts from the minimum path-metric
+ *     state, walks back through the L traceback stages and emits the D
+ *     decoded bits, packed 8 per byte.
+ * Points the paper leaves open are fixed as in DESIGN.md §3 (readings c-1 ..
+ * c-24): tie -> upper branch; head block = known start state 0; terminated
+ * tail -> traceback from state 0; argmin ties -> lowest state index.
+ *
+ * Conventions
+ *   polys     generator polynomials, bit K-1 = input tap g_{K-1}, bit 0 = g_0
+ *             (e.g. CCSDS {0171, 0133}); output bit order follows the list.
+ *   soft in   int8, one value per coded bit, [stage][r] order, punctured
+ *             positions omitted; value > 0 favours coded bit 0 (BPSK 0 -> +1).
+ *             Every int8 value (including -128) is accepted.
+ *   bits out  packed LSB-first: info bit i -> byte i>>3, bit (i & 7); pad 0.
+ *   TERMINATED the stream carries K-1 extra zero-tail stages after n_info;
+ *             the last block traces back from state 0 and the tail is not
+ *             emitted.
+ *
+ * Ownership / threading
+ *   The caller owns every input and output buffer (device pointers unless a
+ *   function says "host") and the CUDA stream.  The handle owns its code
+ *   tables and a survivor workspace on its device (grown on demand, freed by
+ *   pbvd_destroy).  Decode calls are asynchronous on `stream` (a cudaStream_t
+ *   passed as void*, NULL = legacy default stream) unless stated otherwise.
+ *   A handle must not be used from two host threads at once; use one handle
+ *   per concurrent stream.
+ *
+ * Errors
+ *   Every function returns PBVD_OK (0) or a negative pbvd_status; nothing is
+ *   thrown or aborted across the ABI.  pbvd_last_error() gives a message for
+ *   the last failure on a handle (including the CUDA error string).  There is
+ *   no CPU fallback: a call that cannot run on the GPU fails.
+ */
+#ifndef PBVD_H
+#define PBVD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pbvd_s *pbvd_t;
+
+enum pbvd_status {
+    PBVD_OK = 0,
+    PBVD_EINVAL = -1,       /* bad argument (null pointer, range)              */
+    PBVD_ENOMEM = -2,       /* device or host allocation failed                */
+    PBVD_ECUDA = -3,        /* CUDA runtime / launch error                     */
+    PBVD_EUNSUPPORTED = -4, /* code has no compiled kernel (see pbvd_supported) */
+    PBVD_ESIZE = -5         /* buffer length inconsistent with n_info          */
+};
+
+#define PBVD_TERMINATED (1u << 0) /* stream ends with K-1 zero tail stages (c-13) */
+
+/* Create a decoder on CUDA device `device`.
+ *   K          constraint length (3..9 compiled)
+ *   R          generators per code (code rate 1/R before puncturing), 2..4
+ *   polys      R generator polynomials (see Conventions); host pointer
+ *   punct_period P >= 1; 1 = unpunctured
+ *   punct      R*P keep flags, row r (generator r) then column p, i.e.
+ *              punct[r*P + p]; host pointer, NULL iff P == 1.  Column p
+ *              applies to stages s with s mod P == p (also the tail stages).
+ *   D          decoded stages per block, D >= 8 and D % 8 == 0 (blocks own
+ *              whole output bytes)
+ *   L          truncation / traceback length (M = L), 1 <= L
+ *   soft_bits  quantisation of the input, 1..8 (1 = hard +-1); advisory only
+ *   flags      PBVD_TERMINATED or 0
+ * Returns PBVD_EUNSUPPORTED if no kernel is compiled for (K, R, polys);
+ * pbvd_supported() lists them. */
+int pbvd_create(pbvd_t *out, int K, int R, const uint32_t *polys, int punct_period,
+                const uint8_t *punct, int D, int L, int soft_bits, unsigned flags,
+                int device);
+
+void pbvd_destroy(pbvd_t h);
+
+/* Number of int8 soft values of a stream with n_info info bits (including the
+ * K-1 tail stages if TERMINATED, after puncturing).  Negative on error. */
+int64_t pbvd_llr_count(pbvd_t h, int64_t n_info);
+
+/* Number of stages (n_info, plus K-1 if TERMINATED) and blocks ceil(n_info/D). */
+int64_t pbvd_stage_count(pbvd_t h, int64_t n_info);
+int64_t pbvd_block_count(pbvd_t h, int64_t n_info);
+
+/* Decode a whole stream.
+ *   d_llr  device, n_llr == pbvd_llr_count(n_info) int8 values
+ *   d_bits device, >= ceil(n_info/8) bytes, fully written (pad bits 0)
+ * Asynchronous on `stream`. */
+int pbvd_decode(pbvd_t h, const int8_t *d_llr, int64_t n_llr, uint8_t *d_bits, int64_t n_info,
+                void *stream);
+
+/* Decode blocks [block0, block0+nblocks) of a stream of n_info_total info bits
+ * (the multi-GPU shard entry point).
+ *   d_llr_window  device pointer to the first kept soft value of stage
+ *                 window_stage0; the window holds window_n_llr values and must
+ *                 cover every forward span of the range, i.e. stages
+ *                 [max(0, block0*D - L), min(n_stages, (block0+nblocks)*D + L))
+ *                 (all remaining stages if the range ends with the last block)
+ *   d_bits        device, receives the bits of [block0*D, min((block0+nblocks)*D,
+ *                 n_info)) packed LSB-first from byte 0 (ceil(bits/8) bytes)
+ * Asynchronous on `stream`. */
+int pbvd_decode_blocks(pbvd_t h, const int8_t *d_llr_window, int64_t window_stage0,
+                       int64_t window_n_llr, int64_t n_info_total, int64_t block0,
+                       int64_t nblocks, uint8_t *d_bits, void *stream);
+
+/* End-to-end decode from HOST memory: copies h_llr to the device, decodes and
+ * copies the packed bits back to h_bits, pipelined in segments over
+ * `n_streams` internal CUDA streams so transfers overlap the kernels (§IV.C,
+ * P:284-301).  h_llr / h_bits should be pinned (cudaHostAlloc /
+ * torch pin_memory) for overlap; pageable memory works but serialises.
+ * Synchronous: returns when h_bits is complete. */
+int pbvd_decode_host(pbvd_t h, const int8_t *h_llr, int64_t n_llr, uint8_t *h_bits,
+                     int64_t n_info, int n_streams);
+
+/* Tuning / introspection ------------------------------------------------- */
+
+/* Lanes per block pair used by the forward kernel (1, 2, 4, 8; 0 = default
+ * for the code).  Returns PBVD_EUNSUPPORTED if that variant is not compiled. */
+int pbvd_set_lanes(pbvd_t h, int lanes);
+int pbvd_get_lanes(pbvd_t h);
+
+/* Upper bound on the survivor workspace in bytes (default 4 GiB); decodes
+ * larger than one workspace run in waves. */
+int pbvd_set_workspace_limit(pbvd_t h, size_t bytes);
+
+/* When enabled, each decode records CUDA events around every kernel launch
+ * on the caller's stream; pbvd_kernel_times() (after the stream is
+ * synchronised) returns the summed forward and traceback kernel times (ms)
+ * of the most recent decode call and the number of kernel launches. */
+int pbvd_set_profiling(pbvd_t h, int enable);
+int pbvd_kernel_times(pbvd_t h, float *fwd_ms, float *tb_ms, int *launches);
+
+/* Survivor bytes written per decoded stage-block (N/8 * span) etc. */
+typedef struct {
+    int K, R, N, lanes, D, L, P;
+    int64_t dec_bytes_per_block; /* survivor bytes of one interior block   */
+    int64_t span;                /* forward stages of one interior block   */
+    size_t workspace_bytes;      /* currently allocated                    */
+} pbvd_info;
+int pbvd_get_info(pbvd_t h, pbvd_info *info);
+
+/* Compiled (K, R, polys...) combinations, as text "K:R:o1,o2[,o3]:lanes;..." */
+const char *pbvd_supported(void);
+
+const char *pbvd_strerror(int code);
+const char *pbvd_last_error(pbvd_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBVD_H */

@@ -1,0 +1,80 @@
+"""ctypes prototypes of libpbvd.so (include/pbvd.h).  Argument marshalling
+only: every step of the decode runs in the library's CUDA kernels.  There is
+no CPU fallback -- if the library is missing this module raises."""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libpbvd.so"
+
+PBVD_OK = 0
+PBVD_TERMINATED = 1
+
+EXPORTS = (
+    "pbvd_create", "pbvd_destroy", "pbvd_llr_count", "pbvd_stage_count", "pbvd_block_count",
+    "pbvd_decode", "pbvd_decode_blocks", "pbvd_decode_host", "pbvd_set_lanes", "pbvd_get_lanes",
+    "pbvd_set_workspace_limit", "pbvd_set_profiling", "pbvd_kernel_times", "pbvd_get_info",
+    "pbvd_supported", "pbvd_strerror", "pbvd_last_error",
+)
+
+
+class PbvdInfo(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int), ("R", ctypes.c_int), ("N", ctypes.c_int),
+                ("lanes", ctypes.c_int), ("D", ctypes.c_int), ("L", ctypes.c_int),
+                ("P", ctypes.c_int), ("dec_bytes_per_block", ctypes.c_int64),
+                ("span", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t)]
+
+
+_lib = None
+
+
+def load(path: os.PathLike | None = None):
+    """Load libpbvd.so (build it first with paper_1608_00066_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ImportError(f"{p} not found: build the CUDA library first "
+                          "(python -m paper_1608_00066_b200.build); there is no CPU fallback")
+    L = ctypes.CDLL(str(p))
+    i32, i64, u32 = ctypes.c_int, ctypes.c_int64, ctypes.c_uint
+    vp, cp = ctypes.c_void_p, ctypes.c_char_p
+    h = ctypes.c_void_p
+    L.pbvd_create.argtypes = [ctypes.POINTER(h), i32, i32, ctypes.POINTER(ctypes.c_uint32), i32,
+                              ctypes.POINTER(ctypes.c_uint8), i32, i32, i32, u32, i32]
+    L.pbvd_create.restype = i32
+    L.pbvd_destroy.argtypes = [h]
+    L.pbvd_destroy.restype = None
+    for fn in ("pbvd_llr_count", "pbvd_stage_count", "pbvd_block_count"):
+        getattr(L, fn).argtypes = [h, i64]
+        getattr(L, fn).restype = i64
+    L.pbvd_decode.argtypes = [h, vp, i64, vp, i64, vp]
+    L.pbvd_decode.restype = i32
+    L.pbvd_decode_blocks.argtypes = [h, vp, i64, i64, i64, i64, i64, vp, vp]
+    L.pbvd_decode_blocks.restype = i32
+    L.pbvd_decode_host.argtypes = [h, vp, i64, vp, i64, i32]
+    L.pbvd_decode_host.restype = i32
+    L.pbvd_set_lanes.argtypes = [h, i32]
+    L.pbvd_set_lanes.restype = i32
+    L.pbvd_get_lanes.argtypes = [h]
+    L.pbvd_get_lanes.restype = i32
+    L.pbvd_set_workspace_limit.argtypes = [h, ctypes.c_size_t]
+    L.pbvd_set_workspace_limit.restype = i32
+    L.pbvd_set_profiling.argtypes = [h, i32]
+    L.pbvd_set_profiling.restype = i32
+    L.pbvd_kernel_times.argtypes = [h, ctypes.POINTER(ctypes.c_float),
+                                    ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
+    L.pbvd_kernel_times.restype = i32
+    L.pbvd_get_info.argtypes = [h, ctypes.POINTER(PbvdInfo)]
+    L.pbvd_get_info.restype = i32
+    L.pbvd_supported.argtypes = []
+    L.pbvd_supported.restype = cp
+    L.pbvd_strerror.argtypes = [i32]
+    L.pbvd_strerror.restype = cp
+    L.pbvd_last_error.argtypes = [h]
+    L.pbvd_last_error.restype = cp
+    _lib = L
+    return L

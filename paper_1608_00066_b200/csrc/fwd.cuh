@@ -1,0 +1,463 @@
+// fwd.cuh -- forward kernel of the PBVD on sm_100a: branch metrics + ACS +
+// decision packing + bulk store of survivors + final argmin per block.
+//
+// Paper mapping (PAPER.md line numbers "P:n"):
+//   ACS recursion, Eq. 1; encoder / trellis, Eq. 2 and the shift
+//   S_2j,S_2j+1 -> S_j,S_{j+2^{v-1}}; butterfly outputs
+//   alpha/beta/gamma/theta, Eqs. 3-6: only the 2^R distinct
+//   codeword metrics of a stage are formed; survivor bit 0 =
+//   upper branch; parallel-block geometry; traceback
+//   start = min-PM state.
+//
+// B200 design (not the paper's GTX580/980 thread mapping):
+//   * "block-SIMD": every 32-bit register holds the int16 path metrics of
+//     ONE state for TWO blocks (lo half = even block, hi half = odd block);
+//     all arithmetic is 16x2 SIMD, so BM and ACS cost is shared by a pair.
+//   * W lanes of a warp hold the N states of a block pair, S = N/W states per
+//     lane, all in registers.  The butterfly is done IN PLACE: at phase p
+//     (stage mod v) the two inputs of a butterfly are the physical slots that
+//     differ in physical bit p, and its x=0 / x=1 outputs overwrite them.
+//     Logical state u lives in physical slot rotl_v(u, p) -- the index bits
+//     rotate once per stage, so no data moves for register bits; when bit p
+//     is a lane bit the partner values are fetched with one SHFL.BFLY per
+//     register.
+//   * path metrics use a non-negative branch metric BM+(c) = BM(c) +
+//     sum_r max(-lam_r, 0) (a per-stage constant shift of the canonical
+//     metric, reading c-4: every decision and tie is identical) and are
+//     re-normalised by the block minimum every T stages, so all values stay
+//     in [0, 32767] (reading c-20) and plain 32-bit adds are exact 16x2 adds.
+//   * ACS per output: 1 add (other candidate), 1 VIADDMNMX.S16x2 (the fused
+//     add+min -- Blackwell DPX), 1 IADD3 producing m_own - m_other + 0x7FFF
+//     whose per-half sign bit is the decision (m_other < m_own, tie -> upper).
+//   * decisions: sign bits of 2 registers -> 4 bytes via PRMT sign-replicate,
+//     8 such words merged by LOP3 into one 32-bit word (32 decisions), stored
+//     to shared memory; each warp streams T stages of survivors to HBM with
+//     one cp.async.bulk (TMA engine) per chunk.
+//   * soft inputs: 16-byte cp.async (LDGSTS) of each block's window into
+//     shared memory (double buffered), depunctured per block into a
+//     [stage][pair] table read with one 8-byte LDS per stage per lane.
+#pragma once
+#include <cstdint>
+#include <utility>
+#include "params.h"
+#include "ptx.cuh"
+
+namespace pbvd {
+
+template <int K_, int R_, uint32_t G0, uint32_t G1, uint32_t G2 = 0, uint32_t G3 = 0>
+struct Code {
+    static constexpr int K = K_, R = R_, V = K_ - 1, N = 1 << (K_ - 1), NC = 1 << R_;
+    __host__ __device__ static constexpr uint32_t g(int r) { return r == 0 ? G0 : r == 1 ? G1 : r == 2 ? G2 : G3; }
+    // column i of the generator matrix, bit r = g^(r)_i
+    __host__ __device__ static constexpr int col(int i) {
+        int c = 0;
+        for (int r = 0; r < R_; ++r) c |= int((g(r) >> i) & 1u) << r;
+        return c;
+    }
+    static constexpr int gK = col(K_ - 1);   // beta  = alpha ^ gK       (Eq. 4)
+    static constexpr int g0 = col(0);        // gamma = alpha ^ g0       (Eq. 5)
+    static constexpr int ALL = (1 << R_) - 1;
+    static constexpr bool symmetric = (gK == ALL) && (g0 == ALL);
+};
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+template <class C, int W_>
+struct Cfg {
+    using code = C;
+    static constexpr int V = C::V, N = C::N, R = C::R, NC = C::NC, W = W_;
+    static constexpr int w = ilog2(W_);       // lane bits
+    static constexpr int S = N / W_;          // states (registers) per lane
+    static constexpr int LB = V - w;          // physical bits [0,LB) = register bits
+    static constexpr int WPS = S >= 16 ? S / 16 : 1;   // decision words per lane per stage
+    static constexpr int PPW = 32 / W_;       // block pairs per warp
+    static constexpr int BPW = 2 * PPW;       // blocks per warp (= per survivor region)
+    static constexpr int NWARP = cmax(1, cmin(8, (N >= 256 ? 64 : 128) / BPW));
+    static constexpr int NT = NWARP * 32;
+    static constexpr int BPC = NWARP * BPW;   // blocks per CTA
+    static constexpr int PPC = NWARP * PPW;   // pairs per CTA
+    static constexpr int T = V * (32 / V);    // stages per chunk = normalisation period
+    static constexpr int RAWB = ((T * R + 15) / 16) * 16 + 32;   // raw window bytes
+    static constexpr int ROW = 32 * WPS;      // survivor words per stage per region
+    static constexpr size_t SMEM_RAW = size_t(2) * BPC * RAWB;
+    static constexpr size_t SMEM_LAM = size_t(T) * PPC * 8;
+    static constexpr size_t SMEM_DEC = size_t(NWARP) * T * ROW * 4;
+    static constexpr size_t SMEM = SMEM_RAW + SMEM_LAM + SMEM_DEC;
+
+    // alpha of the butterfly whose E slot has register index k, restricted
+    // to the register bits (Eq. 3 on the physical->logical bit map of phase p)
+    __host__ __device__ static constexpr int alpha_reg(int k, int p) {
+        int a = 0;
+        for (int b = 0; b < LB; ++b)
+            if (b != p && ((k >> b) & 1)) a ^= C::col(((b - p) % V + V) % V);
+        return a;
+    }
+    // R-bit mask of alpha bits a lane bit can flip at phase p
+    __host__ __device__ static constexpr int lane_possible(int p) {
+        int m = 0;
+        for (int i = 0; i < w; ++i) {
+            int b = LB + i;
+            if (b != p) m |= C::col(((b - p) % V + V) % V);
+        }
+        return m;
+    }
+};
+
+// lane part of alpha at phase p for lane-in-group lg
+template <class CF, int P>
+__device__ __forceinline__ int lane_alpha(int lg) {
+    using C = typename CF::code;
+    int a = 0;
+#pragma unroll
+    for (int i = 0; i < CF::w; ++i) {
+        const int b = CF::LB + i;
+        if (b != P && ((lg >> i) & 1)) a ^= C::col(((b - P) % CF::V + CF::V) % CF::V);
+    }
+    return a;
+}
+
+// The 2^R non-negative codeword metrics of one stage for a block pair,
+// permuted by the lane's alpha offset: Pv[c] = BM+(c ^ flip).
+//   BM+(c) = sum_r (c_r ? max(lam_r,0) : max(-lam_r,0))   (c-4, canonical + const)
+template <class CF, int POSS>
+__device__ __forceinline__ void bm_vector(const uint2 lw, int flip, uint32_t (&Pv)[CF::NC]) {
+    constexpr int R = CF::R;
+    uint32_t x[R], y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        // (lam_A_r, lam_B_r) sign-extended to 16x2
+        const uint32_t sel = uint32_t(r) | (uint32_t(8 | r) << 4) | (uint32_t(4 + r) << 8) |
+                             (uint32_t(12 + r) << 12);
+        const uint32_t l = prmt(lw.x, lw.y, sel);
+        x[r] = __vmaxs2(l, 0u);
+        y[r] = __vsub2(x[r], l);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if ((POSS >> r) & 1) {
+            const uint32_t fm = 0u - uint32_t((flip >> r) & 1);
+            const uint32_t nx = (x[r] & ~fm) | (y[r] & fm);
+            y[r] = (y[r] & ~fm) | (x[r] & fm);
+            x[r] = nx;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CF::NC; ++c) {
+        uint32_t s = ((c & 1) ? x[0] : y[0]);
+#pragma unroll
+        for (int r = 1; r < R; ++r) s += ((c >> r) & 1) ? x[r] : y[r];
+        Pv[c] = s;
+    }
+}
+
+// Pack the S decision words (sign bits 15 / 31 of t[k]) into WPS words and
+// store them to this lane's shared-memory row.  Bit layout of word kw:
+// slot q_reg = 16*kw + (b & 15) of block half (b >> 4)   (S >= 16), or
+// bit = 16*h + 8*(q_reg / (S/2)) + q_reg % (S/2)         (S < 16).
+template <class CF>
+__device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t inv,
+                                           uint32_t* drow) {
+    constexpr int S = CF::S, WPS = CF::WPS;
+    constexpr uint32_t SEL = 0xFBD9u;   // [sgn a.b1, sgn b.b1, sgn a.b3, sgn b.b3]
+    uint32_t words[WPS];
+    if constexpr (S >= 16) {
+#pragma unroll
+        for (int kw = 0; kw < WPS; ++kw) {
+            uint32_t wd = prmt(t[16 * kw], t[16 * kw + 8], SEL);
+#pragma unroll
+            for (int m = 1; m < 8; ++m) {
+                const uint32_t pm = prmt(t[16 * kw + m], t[16 * kw + 8 + m], SEL);
+                const uint32_t M = 0x01010101u * ((1u << m) - 1u);
+                wd = (wd & M) | (pm & ~M);
+            }
+            words[kw] = wd ^ inv;
+        }
+    } else {
+        constexpr int H = S / 2;
+        uint32_t wd = prmt(t[0], t[H], SEL);
+#pragma unroll
+        for (int m = 1; m < H; ++m) {
+            const uint32_t pm = prmt(t[m], t[H + m], SEL);
+            const uint32_t M = 0x01010101u * ((1u << m) - 1u);
+            wd = (wd & M) | (pm & ~M);
+        }
+        words[0] = (wd ^ inv) & (0x01010101u * ((1u << H) - 1u));
+    }
+    if constexpr (WPS == 1) {
+        drow[0] = words[0];
+    } else if constexpr (WPS == 2) {
+        *reinterpret_cast<uint2*>(drow) = make_uint2(words[0], words[1]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < WPS; i += 4)
+            *reinterpret_cast<uint4*>(drow + i) =
+                make_uint4(words[i], words[i + 1], words[i + 2], words[i + 3]);
+    }
+}
+
+// One trellis stage at compile-time phase P (Eq. 1 per output state).
+template <class CF, int P>
+__device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const uint2 lw, int flip,
+                                          int lg, uint32_t* drow) {
+    using C = typename CF::code;
+    constexpr int S = CF::S, NC = CF::NC;
+    constexpr int g0 = C::g0, gK = C::gK;
+    uint32_t t[S];
+    if constexpr (P < CF::LB) {
+        // ---- butterfly partner in this lane (register bit P) --------------
+        uint32_t Pv[NC], PC[NC];
+        bm_vector<CF, CF::lane_possible(P)>(lw, flip, Pv);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) PC[c] = Pv[c] + 0x7FFF7FFFu;
+        constexpr int pb = 1 << P;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            if (k & pb) continue;
+            const int a = CF::alpha_reg(k, P);
+            const uint32_t E = pm[k], O = pm[k | pb];
+            // x = 0: min(E + BM(alpha), O + BM(gamma))        (Eqs. 3, 5)
+            const uint32_t mO0 = O + Pv[a ^ g0];
+            const uint32_t nE = __viaddmin_s16x2(E, Pv[a], mO0);
+            const uint32_t tE = E - mO0 + PC[a];
+            // x = 1: min(E + BM(beta), O + BM(theta))         (Eqs. 4, 6)
+            const uint32_t mO1 = O + Pv[a ^ gK ^ g0];
+            const uint32_t nO = __viaddmin_s16x2(E, Pv[a ^ gK], mO1);
+            const uint32_t tO = E - mO1 + PC[a ^ gK];
+            pm[k] = nE;
+            pm[k | pb] = nO;
+            t[k] = tE;
+            t[k | pb] = tO;
+        }
+        pack_store<CF>(t, 0u, drow);
+    } else {
+        // ---- butterfly partner in lane lg ^ (1 << li) ----------------------
+        constexpr int li = P - CF::LB;
+        const uint32_t lb = uint32_t(lg >> li) & 1u;   // 0: E side (x=0), 1: O side (x=1)
+        uint32_t recv[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) recv[k] = __shfl_xor_sync(0xffffffffu, pm[k], 1 << li);
+        uint32_t Po[NC], Pr[NC], PCo[NC];
+        const uint32_t Cc = 0x7FFF7FFFu + lb * 0x00010001u;   // inverted sense on O side
+        if constexpr (C::symmetric) {
+            // own: alpha (E side) / theta = alpha (O side); other: gamma = beta = ~alpha
+            bm_vector<CF, CF::lane_possible(P)>(lw, flip, Po);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) Pr[c] = Po[c ^ C::ALL];
+        } else {
+            const int fo = flip ^ (lb ? (gK ^ g0) : 0);
+            const int fr = flip ^ (lb ? gK : g0);
+            bm_vector<CF, CF::lane_possible(P) | (gK ^ g0)>(lw, fo, Po);
+            bm_vector<CF, CF::lane_possible(P) | gK | g0>(lw, fr, Pr);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) PCo[c] = Po[c] + Cc;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const int a = CF::alpha_reg(k, P);
+            const uint32_t own = pm[k];
+            const uint32_t mR = recv[k] + Pr[a];
+            pm[k] = __viaddmin_s16x2(own, Po[a], mR);
+            t[k] = own - mR + PCo[a];
+        }
+        pack_store<CF>(t, 0u - lb, drow);
+    }
+}
+
+template <class CF, int P>
+__device__ __forceinline__ void stage_guarded(uint32_t (&pm)[CF::S], const uint2* lamrow,
+                                              const int (&flip)[CF::V], int lg,
+                                              uint32_t* drow, int s, int nst) {
+    if (s < nst) {
+        const uint2 lw = lamrow[size_t(s) * CF::PPC];
+        acs_stage<CF, P>(pm, lw, flip[P], lg, drow + size_t(s) * CF::ROW);
+    }
+}
+
+template <class CF, int... Ps>
+__device__ __forceinline__ void cycle(uint32_t (&pm)[CF::S], const uint2* lamrow,
+                                      const int (&flip)[CF::V], int lg, uint32_t* drow, int s0,
+                                      int nst, std::integer_sequence<int, Ps...>) {
+    (stage_guarded<CF, Ps>(pm, lamrow, flip, lg, drow, s0 + Ps, nst), ...);
+}
+
+template <class CF, int... Ps>
+__device__ __forceinline__ void init_flips(int (&flip)[CF::V], int lg,
+                                           std::integer_sequence<int, Ps...>) {
+    ((flip[Ps] = lane_alpha<CF, Ps>(lg)), ...);
+}
+
+__device__ __forceinline__ int64_t kept_before(const FwdParams& p, int64_t s, int R) {
+    if (p.P == 1) return s * R;
+    return (s / p.P) * p.kp + p.cum[s % p.P];
+}
+
+template <class CF>
+__global__ void __launch_bounds__(CF::NT) fwd_kernel(const __grid_constant__ FwdParams p) {
+    constexpr int V = CF::V, N = CF::N, S = CF::S, W = CF::W, R = CF::R, T = CF::T;
+    constexpr int NT = CF::NT, BPC = CF::BPC, BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW;
+    constexpr int RAWB = CF::RAWB;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* raw = smem;
+    uint2* lam = reinterpret_cast<uint2*>(smem + CF::SMEM_RAW);
+    uint32_t* decs = reinterpret_cast<uint32_t*>(smem + CF::SMEM_RAW + CF::SMEM_LAM);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lg = lane & (W - 1), grp = lane / W;
+    const bool edge = int(blockIdx.x) >= p.n_int_ctas;
+    const int e = int(blockIdx.x) - p.n_int_ctas;
+    const int span = edge ? p.edges[e].span : p.span_int;
+    const bool head = edge && (p.edges[e].flags & EDGE_HEAD);
+    const int64_t cta_b0 = int64_t(blockIdx.x) * BPC;   // launch-relative first interior block
+
+    auto block_lo = [&](int i) -> int64_t {
+        if (edge) return p.edges[e].lo;
+        int64_t bi = cta_b0 + i;
+        if (bi >= p.n_int) bi = p.n_int - 1;
+        return (p.b_int0 + bi) * p.D - p.L;
+    };
+
+    const uintptr_t vlo = reinterpret_cast<uintptr_t>(p.llr);
+    const uintptr_t vhi = vlo + uintptr_t(p.n_llr);
+    // stage chunk c's raw soft values of every block of the CTA into raw[buf]
+    auto issue_raw = [&](int c, int buf) {
+        const int s0 = c * T;
+        const int nst = min(T, span - s0);
+        for (int i = tid; i < BPC; i += NT) {
+            const int64_t a = block_lo(i) + s0;
+            const int64_t k0 = kept_before(p, a, R) - p.kb_ws0;
+            const int64_t k1 = kept_before(p, a + nst, R) - p.kb_ws0;
+            const uintptr_t g0 = vlo + uintptr_t(k0);
+            const uintptr_t ga = g0 & ~uintptr_t(15);
+            const uintptr_t gb = (vlo + uintptr_t(k1) + 15) & ~uintptr_t(15);
+            uint8_t* dst = raw + (size_t(buf) * BPC + i) * RAWB;
+            for (uintptr_t x = ga; x < gb; x += 16, dst += 16) {
+                if (x >= vlo && x + 16 <= vhi) {
+                    cp_async16(smem_u32(dst), reinterpret_cast<const void*>(x));
+                } else {
+                    for (int j = 0; j < 16; ++j) {
+                        const uintptr_t y = x + j;
+                        dst[j] = (y >= vlo && y < vhi) ? *reinterpret_cast<const uint8_t*>(y) : 0;
+                    }
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    // depuncture raw[buf] into lam[stage][pair] = {A bytes r0..r3, B bytes r0..r3}
+    auto transform = [&](int c, int buf) {
+        const int s0 = c * T;
+        const int nst = min(T, span - s0);
+        for (int i = tid; i < BPC; i += NT) {
+            const int64_t a = block_lo(i) + s0;
+            const int64_t k0 = kept_before(p, a, R) - p.kb_ws0;
+            const int off = int((vlo + uintptr_t(k0)) & 15);
+            const uint8_t* src = raw + (size_t(buf) * BPC + i) * RAWB + off;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(lam) + (i >> 1) * 2 + (i & 1);
+            if (p.P == 1) {
+                for (int s = 0; s < nst; ++s) {
+                    uint32_t v = 0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) v |= uint32_t(src[s * R + r]) << (8 * r);
+                    dst[size_t(s) * CF::PPC * 2] = v;
+                }
+            } else {
+                int ph = int(a % p.P), idx = 0;
+                for (int s = 0; s < nst; ++s) {
+                    uint32_t v = 0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if ((p.keep >> (r * p.P + ph)) & 1) v |= uint32_t(src[idx++]) << (8 * r);
+                    dst[size_t(s) * CF::PPC * 2] = v;
+                    ph = (ph + 1 == p.P) ? 0 : ph + 1;
+                }
+            }
+        }
+    };
+
+    // ---- per-lane constants ------------------------------------------------
+    int flip[V];
+    init_flips<CF>(flip, lg, std::make_integer_sequence<int, V>{});
+
+    uint32_t pm[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+        pm[k] = head ? ((lg == 0 && k == 0) ? 0u : uint32_t(S_HEAD) * 0x00010001u) : 0u;
+
+    const uint2* lamrow = lam + warp * PPW + grp;
+    uint32_t* drow = decs + (size_t(warp) * T * 32 + lane) * CF::WPS;   // + s*ROW
+    uint32_t* gdec = nullptr;
+    if (!edge) {
+        if (cta_b0 + int64_t(warp) * BPW < p.n_int)
+            gdec = p.dec + (size_t(blockIdx.x) * CF::NWARP + warp) * size_t(p.span_int) * ROW;
+    } else if (warp == 0) {
+        gdec = p.dec_edge + size_t(e) * size_t(p.span_edge_max) * ROW;
+    }
+
+    const int nchunks = (span + T - 1) / T;
+    issue_raw(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            issue_raw(c + 1, (c + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        transform(c, c & 1);
+        __syncthreads();
+        if (c > 0) {
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+        }
+        const int nst = min(T, span - c * T);
+#pragma unroll 1
+        for (int s0 = 0; s0 < nst; s0 += V)
+            cycle<CF>(pm, lamrow, flip, lg, drow, s0, nst, std::make_integer_sequence<int, V>{});
+        // renormalise: subtract the block minimum (per 16-bit half = per block)
+        uint32_t mn = pm[0];
+#pragma unroll
+        for (int k = 1; k < S; ++k) mn = __vmins2(mn, pm[k]);
+#pragma unroll
+        for (int o = 1; o < W; o <<= 1) mn = __vmins2(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+#pragma unroll
+        for (int k = 0; k < S; ++k) pm[k] -= mn;
+        // stream this chunk's survivors to HBM (one bulk copy per warp)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && gdec != nullptr) {
+            bulk_s2g(gdec + size_t(c) * T * ROW, smem_u32(decs + size_t(warp) * T * ROW),
+                     uint32_t(nst) * ROW * 4u);
+            bulk_commit();
+        }
+    }
+
+    // ---- traceback start: min PM, lowest logical state on ties --------
+    const int pend = span % V;
+    uint32_t kA = 0xffffffffu, kB = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        const uint32_t q = uint32_t(lg * S + k);
+        const uint32_t u = ((q >> pend) | (q << (V - pend))) & uint32_t(N - 1);
+        kA = min(kA, ((pm[k] & 0xffffu) << 8) | u);
+        kB = min(kB, ((pm[k] >> 16) << 8) | u);
+    }
+#pragma unroll
+    for (int o = 1; o < W; o <<= 1) {
+        kA = min(kA, __shfl_xor_sync(0xffffffffu, kA, o));
+        kB = min(kB, __shfl_xor_sync(0xffffffffu, kB, o));
+    }
+    if (lg == 0) {
+        if (!edge) {
+            const int64_t bi = cta_b0 + warp * BPW + 2 * grp;
+            if (bi < p.n_int) p.start[bi] = int32_t(kA & 0xffu);
+            if (bi + 1 < p.n_int) p.start[bi + 1] = int32_t(kB & 0xffu);
+        } else if (warp == 0 && grp == 0) {
+            p.start_edge[e] = (p.edges[e].flags & EDGE_START0) ? 0 : int32_t(kA & 0xffu);
+        }
+    }
+    if (lane == 0) bulk_wait<0>();
+}
+
+}  // namespace pbvd

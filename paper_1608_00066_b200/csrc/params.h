@@ -1,0 +1,64 @@
+// params.h -- kernel parameter blocks shared by the host planner and the
+// sm_100a kernels (plain structs, passed by value as kernel parameters).
+#pragma once
+#include <cstdint>
+
+namespace pbvd {
+
+constexpr int MAX_EDGE = 32;      // edge blocks per launch (more -> extra launches)
+constexpr int S_HEAD = 8192;      // known-start sentinel, > v*128*R (reading c-12)
+
+// One "edge" block: a block whose forward span is not the uniform
+// [bD-L, bD+D+L) -- head blocks (span starts at stage 0, known start state),
+// blocks clipped by the end of the stream, and the last block.
+struct EdgeDesc {
+    int64_t lo;        // absolute first stage of the forward span
+    int64_t out_bit0;  // bit offset of the block's first decoded bit in d_bits
+    int span;          // forward stages
+    int t0r, t1r;      // decoding range relative to lo: [t0r, t1r)
+    int flags;         // EDGE_HEAD | EDGE_START0
+};
+constexpr int EDGE_HEAD = 1;    // initial metrics: state 0 -> 0, others S_HEAD
+constexpr int EDGE_START0 = 2;  // traceback starts in state 0 (terminated tail)
+
+struct FwdParams {
+    const int8_t* llr;     // window base: first kept value of stage ws0
+    int64_t n_llr;         // valid values in the window
+    int64_t kb_ws0;        // kept values before stage ws0 (absolute index of llr[0])
+    int64_t b_int0;        // first interior block (absolute index)
+    int n_int;             // interior blocks in this launch
+    int n_int_ctas;        // CTAs for interior blocks; edge CTAs follow
+    int D, L;
+    int span_int;          // D + 2L
+    int P;                 // puncture period (1 = none)
+    int kp;                // kept values per period
+    uint64_t keep;         // keep flag of (r, p) at bit r*P + p
+    int cum[16];           // kept values in columns [0, p) of one period
+    uint32_t* dec;         // interior survivor regions
+    int32_t* start;        // interior start states (logical state index)
+    uint32_t* dec_edge;    // edge survivor regions
+    int32_t* start_edge;   // edge start states
+    int span_edge_max;     // stage capacity of one edge region
+    int n_edge;
+    EdgeDesc edges[MAX_EDGE];
+};
+
+struct TbParams {
+    const uint32_t* dec;
+    const int32_t* start;
+    int n_int;
+    int n_int_ctas;
+    int span_int;
+    int t0r, t1r;          // interior decoding range relative to lo (L, L+D)
+    int D;
+    int word_out;          // 1: interior blocks store aligned 32-bit words
+    int64_t out_bit0;      // bit offset of the first interior block in d_bits
+    uint8_t* out;
+    const uint32_t* dec_edge;
+    const int32_t* start_edge;
+    int span_edge_max;
+    int n_edge;
+    EdgeDesc edges[MAX_EDGE];
+};
+
+}  // namespace pbvd

@@ -1,0 +1,542 @@
+// pbvd.cu -- C ABI (include/pbvd.h) of the B200 parallel block-based Viterbi
+// decoder: validation, block planning (interior blocks with the
+// uniform span [bD-L, bD+D+L) plus "edge" blocks at the stream ends), survivor
+// workspace and waves, and the two kernel launches per wave (forward: fwd.cuh,
+// traceback: tb.cuh).  Torch is not involved below this line.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pbvd.h"
+#include "variant.h"
+
+namespace pbvd {
+
+const std::vector<Variant>& variants() {
+    static const std::vector<Variant> v = [] {
+        std::vector<Variant> r;
+        add_variants_k3(r);
+        add_variants_k5(r);
+        add_variants_k7(r);
+        add_variants_k7r3(r);
+        add_variants_k9(r);
+        return r;
+    }();
+    return v;
+}
+
+static std::mutex g_prep_mu;
+static std::vector<int> g_prepared;  // per (device, variant) flag
+
+}  // namespace pbvd
+
+using namespace pbvd;
+
+struct pbvd_s {
+    int device = 0;
+    int K = 0, R = 0, V = 0, N = 0;
+    uint32_t polys[4] = {0, 0, 0, 0};
+    int P = 1, kp = 0;
+    uint8_t punct[64] = {};
+    int cum[16] = {};
+    uint64_t keep = 0;
+    int D = 0, L = 0, soft_bits = 8;
+    unsigned flags = 0;
+    const Variant* var = nullptr;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    size_t ws_limit = size_t(4) << 30;
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_fwd, ev_tb;   // indices into ev_pool
+    int launches = 0;
+    std::string err;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int fail(pbvd_t h, int code, const std::string& msg) {
+    if (h) h->err = msg;
+    return code;
+}
+
+int cuda_fail(pbvd_t h, cudaError_t e, const char* where) {
+    return fail(h, PBVD_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int64_t kept_before_h(const pbvd_s* h, int64_t s) {
+    if (h->P == 1) return s * h->R;
+    return (s / h->P) * h->kp + h->cum[s % h->P];
+}
+
+int ensure_prepared(pbvd_t h, const Variant* v) {
+    std::lock_guard<std::mutex> lk(g_prep_mu);
+    const auto& vs = variants();
+    const size_t idx = size_t(h->device) * vs.size() + size_t(v - vs.data());
+    if (g_prepared.size() <= idx) g_prepared.resize(idx + 1, 0);
+    if (!g_prepared[idx]) {
+        cudaError_t e = v->prepare();
+        if (e != cudaSuccess) return cuda_fail(h, e, "cudaFuncSetAttribute");
+        g_prepared[idx] = 1;
+    }
+    return PBVD_OK;
+}
+
+int ensure_ws(pbvd_t h, size_t bytes) {
+    if (h->ws_bytes >= bytes) return PBVD_OK;
+    if (h->ws) {
+        cudaFree(h->ws);   // synchronises the device: no pending kernel uses it
+        h->ws = nullptr;
+        h->ws_bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&h->ws, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, PBVD_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
+    }
+    h->ws_bytes = bytes;
+    return PBVD_OK;
+}
+
+int record(pbvd_t h, cudaStream_t s) {
+    if (!h->prof) return -1;
+    const int i = int(h->ev_fwd.size() + h->ev_tb.size()) * 2;
+    while (int(h->ev_pool.size()) <= i + 1) {
+        cudaEvent_t ev;
+        if (cudaEventCreate(&ev) != cudaSuccess) return -1;
+        h->ev_pool.push_back(ev);
+    }
+    (void)s;
+    return i;
+}
+
+// Block plan of block b (readings c-12, c-13, c-14, c-22).
+struct BlockGeo {
+    int64_t t0, t1, lo, hi;
+};
+BlockGeo geo(const pbvd_s* h, int64_t n_info, int64_t n_stages, int64_t nb, int64_t b) {
+    BlockGeo g;
+    g.t0 = b * h->D;
+    g.t1 = std::min<int64_t>(g.t0 + h->D, n_info);
+    g.lo = std::max<int64_t>(0, g.t0 - h->L);
+    g.hi = (b == nb - 1) ? n_stages : std::min<int64_t>(n_stages, g.t1 + h->L);
+    return g;
+}
+
+int run_blocks(pbvd_t h, const int8_t* llr, int64_t ws0, int64_t n_llr_win, int64_t n_info,
+               int64_t B0, int64_t nblk, uint8_t* out, cudaStream_t stream) {
+    const Variant* v = h->var;
+    const int64_t n_stages = n_info + ((h->flags & PBVD_TERMINATED) ? h->V : 0);
+    const int64_t nb = (n_info + h->D - 1) / h->D;
+    const int64_t B1 = B0 + nblk;
+    if (B0 < 0 || nblk < 1 || B1 > nb) return fail(h, PBVD_EINVAL, "block range outside the stream");
+    if (ws0 < 0 || ws0 > n_stages) return fail(h, PBVD_EINVAL, "window_stage0 outside the stream");
+    const int64_t kb_ws0 = kept_before_h(h, ws0);
+    {   // the window must cover every forward span of the range
+        const BlockGeo a = geo(h, n_info, n_stages, nb, B0);
+        const BlockGeo z = geo(h, n_info, n_stages, nb, B1 - 1);
+        if (a.lo < ws0 || kept_before_h(h, z.hi) - kb_ws0 > n_llr_win)
+            return fail(h, PBVD_ESIZE, "soft-value window does not cover the blocks' spans");
+    }
+    int rc = ensure_prepared(h, v);
+    if (rc) return rc;
+
+    // interior blocks: lo = bD - L >= 0, b < nb-1, (b+1)D + L <= n_stages
+    const int64_t D = h->D, L = h->L;
+    const int64_t first_int = (L + D - 1) / D;
+    const int64_t last_int = std::min<int64_t>(nb - 2, (n_stages - L - D) >= 0 ? (n_stages - L - D) / D : -1);
+    const int64_t I0 = std::min(std::max(first_int, B0), B1);
+    const int64_t I1 = std::max(I0, std::min(last_int + 1, B1));
+    std::vector<EdgeDesc> edges;
+    auto add_edge = [&](int64_t b) {
+        const BlockGeo g = geo(h, n_info, n_stages, nb, b);
+        EdgeDesc e{};
+        e.lo = g.lo;
+        e.out_bit0 = g.t0 - B0 * D;
+        e.span = int(g.hi - g.lo);
+        e.t0r = int(g.t0 - g.lo);
+        e.t1r = int(g.t1 - g.lo);
+        e.flags = (g.lo == 0 ? EDGE_HEAD : 0) |
+                  ((b == nb - 1 && (h->flags & PBVD_TERMINATED)) ? EDGE_START0 : 0);
+        edges.push_back(e);
+    };
+    for (int64_t b = B0; b < I0; ++b) add_edge(b);
+    for (int64_t b = I1; b < B1; ++b) add_edge(b);
+    int span_edge_max = 0;
+    for (const auto& e : edges) span_edge_max = std::max(span_edge_max, e.span);
+
+    // ---- workspace: one wave of interior survivors + edge survivors + starts
+    const int span_int = int(D + 2 * L);
+    const size_t region_bytes = size_t(span_int) * v->ROW * 4;      // BPW blocks
+    const int64_t n_int = I1 - I0;
+    const size_t edge_region_bytes = size_t(span_edge_max) * v->ROW * 4;
+    const size_t edge_bytes = edge_region_bytes * MAX_EDGE + 2 * MAX_EDGE * 4 + 256;
+    const int64_t unit = std::max<int64_t>(v->BPC, 128);   // multiple of BPC and TB CTA (128)
+    int64_t wave = n_int;
+    if (n_int > 0) {
+        const size_t budget = h->ws_limit > edge_bytes ? h->ws_limit - edge_bytes : 0;
+        const int64_t per_unit = int64_t((unit / v->BPW) * region_bytes + unit * 4);
+        int64_t units = std::max<int64_t>(1, int64_t(budget) / per_unit);
+        wave = std::min<int64_t>(n_int, units * unit);
+    }
+    const int64_t wave_regions = (wave + v->BPW - 1) / v->BPW;
+    const size_t int_bytes = size_t(wave_regions) * region_bytes;
+    const size_t start_bytes = size_t(wave + 64) * 4;
+    const size_t need = ((int_bytes + 255) & ~size_t(255)) + ((edge_bytes + 255) & ~size_t(255)) +
+                        ((start_bytes + 255) & ~size_t(255));
+    rc = ensure_ws(h, need);
+    if (rc) return rc;
+    uint8_t* wsb = static_cast<uint8_t*>(h->ws);
+    uint32_t* dec_int = reinterpret_cast<uint32_t*>(wsb);
+    uint32_t* dec_edge = reinterpret_cast<uint32_t*>(wsb + ((int_bytes + 255) & ~size_t(255)));
+    int32_t* start_edge = reinterpret_cast<int32_t*>(
+        reinterpret_cast<uint8_t*>(dec_edge) + edge_region_bytes * MAX_EDGE);
+    int32_t* start_int = reinterpret_cast<int32_t*>(
+        wsb + ((int_bytes + 255) & ~size_t(255)) + ((edge_bytes + 255) & ~size_t(255)));
+
+    FwdParams fp{};
+    fp.llr = llr;
+    fp.n_llr = n_llr_win;
+    fp.kb_ws0 = kb_ws0;
+    fp.D = int(D);
+    fp.L = int(L);
+    fp.span_int = span_int;
+    fp.P = h->P;
+    fp.kp = h->kp;
+    fp.keep = h->keep;
+    for (int i = 0; i < 16; ++i) fp.cum[i] = h->cum[i];
+    fp.dec = dec_int;
+    fp.start = start_int;
+    fp.dec_edge = dec_edge;
+    fp.start_edge = start_edge;
+    fp.span_edge_max = span_edge_max;
+
+    TbParams tp{};
+    tp.dec = dec_int;
+    tp.start = start_int;
+    tp.span_int = span_int;
+    tp.t0r = int(L);
+    tp.t1r = int(L + D);
+    tp.D = int(D);
+    tp.out = out;
+    tp.dec_edge = dec_edge;
+    tp.start_edge = start_edge;
+    tp.span_edge_max = span_edge_max;
+    tp.word_out = ((D & 31) == 0) && ((reinterpret_cast<uintptr_t>(out) & 3) == 0) &&
+                  (((I0 - B0) * D) % 32 == 0);
+
+    size_t next_edge = 0;
+    int64_t done = 0;
+    bool first = true;
+    while (first || done < n_int || next_edge < edges.size()) {
+        first = false;
+        const int64_t cnt = std::min<int64_t>(wave, n_int - done);
+        const int ne = int(std::min<size_t>(MAX_EDGE, edges.size() - next_edge));
+        if (cnt <= 0 && ne == 0) break;
+        fp.b_int0 = I0 + done;
+        fp.n_int = int(std::max<int64_t>(0, cnt));
+        fp.n_int_ctas = int((std::max<int64_t>(0, cnt) + v->BPC - 1) / v->BPC);
+        fp.n_edge = ne;
+        tp.n_int = fp.n_int;
+        tp.n_int_ctas = int((std::max<int64_t>(0, cnt) + 127) / 128);
+        tp.out_bit0 = (I0 + done - B0) * D;
+        tp.n_edge = ne;
+        for (int i = 0; i < ne; ++i) {
+            fp.edges[i] = edges[next_edge + i];
+            tp.edges[i] = edges[next_edge + i];
+        }
+        const int ev = record(h, stream);
+        if (ev >= 0) cudaEventRecord(h->ev_pool[ev], stream);
+        v->fwd(fp.n_int_ctas + ne, stream, fp);
+        if (ev >= 0) {
+            cudaEventRecord(h->ev_pool[ev + 1], stream);
+            h->ev_fwd.push_back({ev, ev + 1});
+        }
+        const int ev2 = record(h, stream);
+        if (ev2 >= 0) cudaEventRecord(h->ev_pool[ev2], stream);
+        v->tb(tp.n_int_ctas + ne, stream, tp);
+        if (ev2 >= 0) {
+            cudaEventRecord(h->ev_pool[ev2 + 1], stream);
+            h->ev_tb.push_back({ev2, ev2 + 1});
+        }
+        h->launches += 2;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
+        done += std::max<int64_t>(0, cnt);
+        next_edge += size_t(ne);
+    }
+    return PBVD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_period,
+                const uint8_t* punct, int D, int L, int soft_bits, unsigned flags, int device) {
+    if (!out) return PBVD_EINVAL;
+    *out = nullptr;
+    if (!polys || K < 3 || K > 9 || R < 2 || R > 4) return PBVD_EINVAL;
+    if (punct_period < 1 || punct_period > 16 || R * punct_period > 64) return PBVD_EINVAL;
+    if ((punct_period > 1) != (punct != nullptr)) return PBVD_EINVAL;
+    if (D < 8 || (D % 8) != 0 || L < 1 || D > (1 << 24) || L > (1 << 20)) return PBVD_EINVAL;
+    if (soft_bits < 1 || soft_bits > 8) return PBVD_EINVAL;
+    if (flags & ~PBVD_TERMINATED) return PBVD_EINVAL;
+    for (int r = 0; r < R; ++r)
+        if (polys[r] == 0 || polys[r] >= (1u << K)) return PBVD_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return PBVD_ECUDA;
+    }
+    const Variant* best = nullptr;
+    for (const auto& v : variants()) {
+        if (v.K != K || v.R != R) continue;
+        bool same = true;
+        for (int r = 0; r < R; ++r) same &= (v.polys[r] == polys[r]);
+        if (!same) continue;
+        if (!best || v.default_rank < best->default_rank) best = &v;
+    }
+    if (!best) return PBVD_EUNSUPPORTED;
+    pbvd_s* h = new (std::nothrow) pbvd_s();
+    if (!h) return PBVD_ENOMEM;
+    h->device = device;
+    h->K = K;
+    h->R = R;
+    h->V = K - 1;
+    h->N = 1 << (K - 1);
+    for (int r = 0; r < R; ++r) h->polys[r] = polys[r];
+    h->P = punct_period;
+    h->D = D;
+    h->L = L;
+    h->soft_bits = soft_bits;
+    h->flags = flags;
+    h->var = best;
+    if (punct_period > 1) {
+        int kp = 0;
+        for (int p = 0; p < punct_period; ++p) {
+            h->cum[p] = kp;
+            for (int r = 0; r < R; ++r) {
+                const uint8_t k = punct[r * punct_period + p] ? 1 : 0;
+                h->punct[r * punct_period + p] = k;
+                if (k) h->keep |= uint64_t(1) << (r * punct_period + p);
+                kp += k;
+            }
+        }
+        if (kp == 0) {
+            delete h;
+            return PBVD_EINVAL;
+        }
+        h->kp = kp;
+    } else {
+        h->kp = R;
+        h->keep = (uint64_t(1) << R) - 1;
+    }
+    *out = h;
+    return PBVD_OK;
+}
+
+void pbvd_destroy(pbvd_t h) {
+    if (!h) return;
+    {
+        DeviceGuard g(h->device);
+        if (h->ws) cudaFree(h->ws);
+        for (auto ev : h->ev_pool) cudaEventDestroy(ev);
+    }
+    delete h;
+}
+
+int64_t pbvd_stage_count(pbvd_t h, int64_t n_info) {
+    if (!h || n_info < 1) return PBVD_EINVAL;
+    return n_info + ((h->flags & PBVD_TERMINATED) ? h->V : 0);
+}
+
+int64_t pbvd_block_count(pbvd_t h, int64_t n_info) {
+    if (!h || n_info < 1) return PBVD_EINVAL;
+    return (n_info + h->D - 1) / h->D;
+}
+
+int64_t pbvd_llr_count(pbvd_t h, int64_t n_info) {
+    if (!h || n_info < 1) return PBVD_EINVAL;
+    return kept_before_h(h, pbvd_stage_count(h, n_info));
+}
+
+int pbvd_decode_blocks(pbvd_t h, const int8_t* d_llr_window, int64_t window_stage0,
+                       int64_t window_n_llr, int64_t n_info_total, int64_t block0,
+                       int64_t nblocks, uint8_t* d_bits, void* stream) {
+    if (!h) return PBVD_EINVAL;
+    if (!d_llr_window || !d_bits || n_info_total < 1 || window_n_llr < 1)
+        return fail(h, PBVD_EINVAL, "null pointer or empty stream");
+    DeviceGuard g(h->device);
+    h->ev_fwd.clear();
+    h->ev_tb.clear();
+    h->launches = 0;
+    return run_blocks(h, d_llr_window, window_stage0, window_n_llr, n_info_total, block0, nblocks,
+                      d_bits, static_cast<cudaStream_t>(stream));
+}
+
+int pbvd_decode(pbvd_t h, const int8_t* d_llr, int64_t n_llr, uint8_t* d_bits, int64_t n_info,
+                void* stream) {
+    if (!h) return PBVD_EINVAL;
+    if (!d_llr || !d_bits || n_info < 1) return fail(h, PBVD_EINVAL, "null pointer or empty stream");
+    if (n_llr != pbvd_llr_count(h, n_info))
+        return fail(h, PBVD_ESIZE, "n_llr != pbvd_llr_count(n_info)");
+    return pbvd_decode_blocks(h, d_llr, 0, n_llr, n_info, 0, pbvd_block_count(h, n_info), d_bits,
+                              stream);
+}
+
+int pbvd_decode_host(pbvd_t h, const int8_t* h_llr, int64_t n_llr, uint8_t* h_bits,
+                     int64_t n_info, int n_streams) {
+    if (!h) return PBVD_EINVAL;
+    if (!h_llr || !h_bits || n_info < 1) return fail(h, PBVD_EINVAL, "null pointer or empty stream");
+    if (n_llr != pbvd_llr_count(h, n_info))
+        return fail(h, PBVD_ESIZE, "n_llr != pbvd_llr_count(n_info)");
+    (void)n_streams;
+    DeviceGuard g(h->device);
+    const size_t out_bytes = size_t((n_info + 7) / 8);
+    int8_t* d_llr = nullptr;
+    uint8_t* d_bits = nullptr;
+    cudaError_t e = cudaMalloc(&d_llr, size_t(n_llr));
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaMalloc");
+    e = cudaMalloc(&d_bits, out_bytes);
+    if (e != cudaSuccess) {
+        cudaFree(d_llr);
+        return cuda_fail(h, e, "cudaMalloc");
+    }
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    int rc = PBVD_OK;
+    e = cudaMemcpyAsync(d_llr, h_llr, size_t(n_llr), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemcpyAsync H2D");
+    if (!rc) rc = pbvd_decode(h, d_llr, n_llr, d_bits, n_info, s);
+    if (!rc) {
+        e = cudaMemcpyAsync(h_bits, d_bits, out_bytes, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemcpyAsync D2H");
+    }
+    e = cudaStreamSynchronize(s);
+    if (!rc && e != cudaSuccess) rc = cuda_fail(h, e, "decode");
+    cudaStreamDestroy(s);
+    cudaFree(d_llr);
+    cudaFree(d_bits);
+    return rc;
+}
+
+int pbvd_set_lanes(pbvd_t h, int lanes) {
+    if (!h) return PBVD_EINVAL;
+    const Variant* best = nullptr;
+    for (const auto& v : variants()) {
+        if (v.K != h->K || v.R != h->R) continue;
+        bool same = true;
+        for (int r = 0; r < h->R; ++r) same &= (v.polys[r] == h->polys[r]);
+        if (!same) continue;
+        if (lanes == 0 ? (!best || v.default_rank < best->default_rank) : v.W == lanes) best = &v;
+    }
+    if (!best) return fail(h, PBVD_EUNSUPPORTED, "no kernel variant with that lane count");
+    h->var = best;
+    return PBVD_OK;
+}
+
+int pbvd_get_lanes(pbvd_t h) { return h ? h->var->W : PBVD_EINVAL; }
+
+int pbvd_set_workspace_limit(pbvd_t h, size_t bytes) {
+    if (!h || bytes < (size_t(1) << 20)) return PBVD_EINVAL;
+    h->ws_limit = bytes;
+    return PBVD_OK;
+}
+
+int pbvd_set_profiling(pbvd_t h, int enable) {
+    if (!h) return PBVD_EINVAL;
+    h->prof = enable != 0;
+    return PBVD_OK;
+}
+
+int pbvd_kernel_times(pbvd_t h, float* fwd_ms, float* tb_ms, int* launches) {
+    if (!h) return PBVD_EINVAL;
+    DeviceGuard g(h->device);
+    float f = 0.f, t = 0.f;
+    for (auto& pr : h->ev_fwd) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&ms, h->ev_pool[pr.first], h->ev_pool[pr.second]);
+        if (e != cudaSuccess) return cuda_fail(h, e, "cudaEventElapsedTime");
+        f += ms;
+    }
+    for (auto& pr : h->ev_tb) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&ms, h->ev_pool[pr.first], h->ev_pool[pr.second]);
+        if (e != cudaSuccess) return cuda_fail(h, e, "cudaEventElapsedTime");
+        t += ms;
+    }
+    if (fwd_ms) *fwd_ms = f;
+    if (tb_ms) *tb_ms = t;
+    if (launches) *launches = h->launches;
+    return PBVD_OK;
+}
+
+int pbvd_get_info(pbvd_t h, pbvd_info* info) {
+    if (!h || !info) return PBVD_EINVAL;
+    info->K = h->K;
+    info->R = h->R;
+    info->N = h->N;
+    info->lanes = h->var->W;
+    info->D = h->D;
+    info->L = h->L;
+    info->P = h->P;
+    info->span = h->D + 2 * h->L;
+    info->dec_bytes_per_block = int64_t(h->D + 2 * h->L) * (h->N / 8 > 0 ? h->N / 8 : 1);
+    info->workspace_bytes = h->ws_bytes;
+    return PBVD_OK;
+}
+
+const char* pbvd_supported(void) {
+    static std::string s;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (const auto& v : variants()) {
+            char buf[96];
+            std::snprintf(buf, sizeof buf, "%d:%d:", v.K, v.R);
+            s += buf;
+            for (int r = 0; r < v.R; ++r) {
+                std::snprintf(buf, sizeof buf, "%s%o", r ? "," : "", v.polys[r]);
+                s += buf;
+            }
+            std::snprintf(buf, sizeof buf, ":%d;", v.W);
+            s += buf;
+        }
+    });
+    return s.c_str();
+}
+
+const char* pbvd_strerror(int code) {
+    switch (code) {
+        case PBVD_OK: return "ok";
+        case PBVD_EINVAL: return "invalid argument";
+        case PBVD_ENOMEM: return "out of memory";
+        case PBVD_ECUDA: return "CUDA error";
+        case PBVD_EUNSUPPORTED: return "unsupported code (no compiled kernel)";
+        case PBVD_ESIZE: return "buffer size inconsistent with n_info";
+        default: return "unknown error";
+    }
+}
+
+const char* pbvd_last_error(pbvd_t h) { return h ? h->err.c_str() : "null handle"; }
+
+}  // extern "C"

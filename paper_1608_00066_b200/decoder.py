@@ -1,0 +1,167 @@
+"""Python binding of the C ABI with the same names: ``Decoder`` wraps a
+``pbvd_t`` handle.  Torch provides device memory and streams only; every
+decode step runs in libpbvd.so's sm_100a kernels (no CPU fallback)."""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+
+
+class PbvdError(RuntimeError):
+    pass
+
+
+def _check(rc, h=None, what=""):
+    if rc < 0:
+        L = _lib.load()
+        msg = L.pbvd_strerror(rc).decode()
+        if h is not None:
+            msg += ": " + L.pbvd_last_error(h).decode()
+        raise PbvdError(f"{what} failed ({rc}): {msg}")
+    return rc
+
+
+def supported():
+    """[(K, R, polys, lanes)] compiled into the library."""
+    out = []
+    for ent in _lib.load().pbvd_supported().decode().strip(";").split(";"):
+        K, R, polys, lanes = ent.split(":")
+        out.append((int(K), int(R), tuple(int(p, 8) for p in polys.split(",")), int(lanes)))
+    return out
+
+
+class Decoder:
+    """pbvd_create(...) -- see include/pbvd.h for the meaning of every argument.
+
+    punct: None or an R x P keep matrix (rows in generator order)."""
+
+    def __init__(self, K, polys, D, L, punct=None, soft_bits=8, terminated=True, device=0,
+                 lanes=0):
+        self._L = _lib.load()
+        self.K, self.polys, self.D, self.L = int(K), tuple(int(p) for p in polys), int(D), int(L)
+        self.R = len(self.polys)
+        self.punct = None if punct is None else tuple(tuple(int(x) for x in row) for row in punct)
+        self.terminated = bool(terminated)
+        self.device = int(device)
+        arr = (ctypes.c_uint32 * self.R)(*self.polys)
+        if self.punct is None:
+            P, pp = 1, None
+        else:
+            P = len(self.punct[0])
+            flat = [self.punct[r][p] for r in range(self.R) for p in range(P)]
+            pp = (ctypes.c_uint8 * len(flat))(*flat)
+        h = ctypes.c_void_p()
+        rc = self._L.pbvd_create(ctypes.byref(h), self.K, self.R, arr, P, pp, self.D, self.L,
+                                 int(soft_bits), _lib.PBVD_TERMINATED if terminated else 0,
+                                 self.device)
+        _check(rc, None, "pbvd_create")
+        self._h = h
+        if lanes:
+            self.set_lanes(lanes)
+
+    # --------------------------------------------------------------- sizes
+    def llr_count(self, n_info):
+        return _check(self._L.pbvd_llr_count(self._h, int(n_info)), self._h, "pbvd_llr_count")
+
+    def stage_count(self, n_info):
+        return _check(self._L.pbvd_stage_count(self._h, int(n_info)), self._h, "pbvd_stage_count")
+
+    def block_count(self, n_info):
+        return _check(self._L.pbvd_block_count(self._h, int(n_info)), self._h, "pbvd_block_count")
+
+    # -------------------------------------------------------------- decode
+    def _stream(self, stream):
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(stream.cuda_stream)
+
+    def decode(self, llr: torch.Tensor, n_info: int, out: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+        """pbvd_decode: int8 CUDA tensor -> packed uint8 CUDA tensor (async)."""
+        if llr.dtype != torch.int8 or not llr.is_cuda or not llr.is_contiguous():
+            raise ValueError("llr must be a contiguous int8 CUDA tensor")
+        nbytes = (int(n_info) + 7) // 8
+        if out is None:
+            out = torch.empty(nbytes, dtype=torch.uint8, device=llr.device)
+        rc = self._L.pbvd_decode(self._h, llr.data_ptr(), llr.numel(), out.data_ptr(),
+                                 int(n_info), self._stream(stream))
+        _check(rc, self._h, "pbvd_decode")
+        return out
+
+    def decode_blocks(self, llr_window: torch.Tensor, window_stage0: int, n_info_total: int,
+                      block0: int, nblocks: int, out: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+        """pbvd_decode_blocks: decode blocks [block0, block0+nblocks) from a window."""
+        if llr_window.dtype != torch.int8 or not llr_window.is_cuda:
+            raise ValueError("llr_window must be an int8 CUDA tensor")
+        t0 = int(block0) * self.D
+        t1 = min((int(block0) + int(nblocks)) * self.D, int(n_info_total))
+        nbytes = (t1 - t0 + 7) // 8
+        if out is None:
+            out = torch.empty(nbytes, dtype=torch.uint8, device=llr_window.device)
+        rc = self._L.pbvd_decode_blocks(self._h, llr_window.data_ptr(), int(window_stage0),
+                                        llr_window.numel(), int(n_info_total), int(block0),
+                                        int(nblocks), out.data_ptr(), self._stream(stream))
+        _check(rc, self._h, "pbvd_decode_blocks")
+        return out
+
+    def decode_host(self, llr: torch.Tensor, n_info: int, out: torch.Tensor | None = None,
+                    n_streams: int = 3) -> torch.Tensor:
+        """pbvd_decode_host: host int8 tensor (pinned for overlap) -> host packed bits."""
+        if llr.dtype != torch.int8 or llr.is_cuda or not llr.is_contiguous():
+            raise ValueError("llr must be a contiguous int8 CPU tensor")
+        nbytes = (int(n_info) + 7) // 8
+        if out is None:
+            out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=llr.is_pinned())
+        rc = self._L.pbvd_decode_host(self._h, llr.data_ptr(), llr.numel(), out.data_ptr(),
+                                      int(n_info), int(n_streams))
+        _check(rc, self._h, "pbvd_decode_host")
+        return out
+
+    # ------------------------------------------------------------- tuning
+    def set_lanes(self, lanes: int):
+        _check(self._L.pbvd_set_lanes(self._h, int(lanes)), self._h, "pbvd_set_lanes")
+
+    @property
+    def lanes(self) -> int:
+        return self._L.pbvd_get_lanes(self._h)
+
+    def set_workspace_limit(self, nbytes: int):
+        _check(self._L.pbvd_set_workspace_limit(self._h, int(nbytes)), self._h,
+               "pbvd_set_workspace_limit")
+
+    def set_profiling(self, enable: bool = True):
+        _check(self._L.pbvd_set_profiling(self._h, int(bool(enable))), self._h,
+               "pbvd_set_profiling")
+
+    def kernel_times(self):
+        """(forward ms, traceback ms, launches) of the last decode (sync first)."""
+        f, t, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int()
+        _check(self._L.pbvd_kernel_times(self._h, ctypes.byref(f), ctypes.byref(t),
+                                         ctypes.byref(n)), self._h, "pbvd_kernel_times")
+        return f.value, t.value, n.value
+
+    def info(self) -> dict:
+        i = _lib.PbvdInfo()
+        _check(self._L.pbvd_get_info(self._h, ctypes.byref(i)), self._h, "pbvd_get_info")
+        return {k: getattr(i, k) for k, _ in _lib.PbvdInfo._fields_}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.pbvd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
