@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the PBVD hot path on B200 (contract: see DESIGN.md §7).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference          # the CPU oracle arm
+
+A step = one pass of the whole hot path (block plan, soft
+input fetch + depuncture, branch metrics, ACS, normalisation, decision
+packing/store, min-PM start, traceback, output packing, and the final gather
+for N > 1) over one batch of synthetic input already resident in HBM.
+Default workload: BASELINE config C2 (K=7 (171,133), rate 1/2, 8-bit soft,
+2^24 info bits, D=512, L=42) per GPU; for N GPUs the stream has N x 2^24
+bits and rank r decodes its contiguous block range (weak scaling).
+`--workload C5` runs the 2^32-bit stream sharded over the GPUs (strong).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
+UNIT = "Gb/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=list(synth.CONFIGS))
+    ap.add_argument("--lanes", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0,
+                    help="target wall time of the cpu_baseline oracle sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def workload(name, world):
+    c = dict(synth.CONFIGS[name])
+    c["name"] = name
+    code, punct = synth.CODES[c["code"]], synth.PUNCT[c["punct"]]
+    if name == "C5":
+        n_total, scaling = c["n_info"], "strong"
+    else:
+        n_total, scaling = c["n_info"] * world, "weak"
+    return c, code, punct, n_total, scaling
+
+
+def describe(c, code, n_total, world):
+    K, R = code["K"], len(code["polys"])
+    polys = ",".join(f"{p:o}" for p in code["polys"])
+    soft = "hard" if c["hard"] else "soft 8-bit"
+    return (f"{c['name']}: K={K} ({polys}) rate {c['punct'] if c['punct'] != '1/2' else '1/' + str(R)}"
+            f" {soft} AWGN {c['ebn0']} dB, {n_total} info bits over {world} GPU(s), "
+            f"D={c['D']} L={c['L']}, terminated")
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while running."""
+
+    def __init__(self, device_index, period=0.005):
+        self.period, self.samples, self.reasons = period, [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def acs_per_block_span(n_info, D, L, K, terminated, b0, nblk):
+    """Sum over blocks of (forward span) x N: the ACS the step performs."""
+    N = 1 << (K - 1)
+    n_stages = n_info + ((K - 1) if terminated else 0)
+    nb = -(-n_info // D)
+    total = 0
+    # interior blocks all have span D + 2L; edge blocks are counted exactly
+    first_int = -(-L // D)
+    last_int = min(nb - 2, (n_stages - L - D) // D if n_stages - L - D >= 0 else -1)
+    lo_i, hi_i = max(first_int, b0), min(last_int + 1, b0 + nblk)
+    n_int = max(0, hi_i - lo_i)
+    total += n_int * (D + 2 * L) * N
+    for b in list(range(b0, min(lo_i, b0 + nblk))) + list(range(max(hi_i, b0), b0 + nblk)):
+        t0 = b * D
+        t1 = min(t0 + D, n_info)
+        lo = max(0, t0 - L)
+        hi = n_stages if b == nb - 1 else min(n_stages, t1 + L)
+        total += (hi - lo) * N
+    return total
+
+
+def load_traffic():
+    """dram bytes per forward launch from the committed ncu summary, if any."""
+    p = ROOT / "profiles" / "latest_fwd_ncu.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("dram_bytes_per_launch"), d
+        except Exception:
+            pass
+    return None, None
+
+
+def cpu_oracle_sample(code, punct, c, llr_host, n_info, target_s, ws0=0, b_first=0,
+                      max_blocks=None):
+    """Time the oracle, as it stands, on a bounded sample of blocks."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    flags = O.TERMINATED
+    nb = -(-n_info // c["D"])
+    if max_blocks is not None:
+        nb = min(nb, b_first + max_blocks)
+    # calibrate on a small sample, then size the measured one
+    cal = min(nb - b_first, max(threads * 4, 64))
+    t = time.perf_counter()
+    O.decode(code, llr_host, n_info, c["D"], c["L"], flags=flags, punct=punct, threads=threads,
+             b0=b_first, nblk=cal, window_stage0=ws0)
+    dt = max(time.perf_counter() - t, 1e-4)
+    nblk = int(min(nb - b_first, max(cal, cal * target_s / dt)))
+    t = time.perf_counter()
+    O.decode(code, llr_host, n_info, c["D"], c["L"], flags=flags, punct=punct, threads=threads,
+             b0=b_first, nblk=nblk, window_stage0=ws0)
+    dt = time.perf_counter() - t
+    bits = min((b_first + nblk) * c["D"], n_info) - b_first * c["D"]
+    return {"value": bits / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{nblk} of {nb} blocks ({bits} info bits) of the same stream, "
+                      f"{threads} pthreads, {dt:.2f} s wall"}
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args):
+    """The oracle arm: the CPU oracle as it stands on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    world = max(1, args.gpus)
+    c, code, punct, n_total, scaling = workload(args.workload, world)
+    # one rank's share of the stream, generated on the host
+    from paper_1608_00066_b200 import shard as S
+    sh = S.plan(n_total, c["D"], c["L"], code["K"], True, world, 0)
+    llr = synth.make_window(code, n_total, c["ebn0"], c["seed"], sh.stage0, sh.stage1, punct,
+                            c["hard"], device="cpu").numpy()
+    from oracle import oracle as O
+    O.build()
+    per_step = max(0.2, min(2.0, 120.0 / max(1, args.steps + args.warmup)))
+    vals, samples = [], None
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(code, punct, c, llr, n_total, per_step, ws0=sh.stage0,
+                              b_first=sh.block0, max_blocks=sh.nblocks)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            samples = r
+    v = statistics.median(vals)
+    cb = dict(samples)
+    cb["value"] = v
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": {"workload": describe(c, code, n_total, world),
+                                         "impl": "CPU oracle (oracle/pbvd_oracle.c), per-edge ACS"},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch.distributed as dist
+    from paper_1608_00066_b200 import build
+    build.build()
+    import paper_1608_00066_b200 as P
+    from paper_1608_00066_b200 import shard as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    c, code, punct, n_total, scaling = workload(args.workload, world)
+    D, L, K = c["D"], c["L"], code["K"]
+    sh = S.plan(n_total, D, L, K, True, world, rank)
+    llr = synth.make_window(code, n_total, c["ebn0"], c["seed"], sh.stage0, sh.stage1, punct,
+                            c["hard"], device=dev)
+    dec = P.Decoder(K, code["polys"], D, L, punct=punct, terminated=True, device=local,
+                    lanes=args.lanes)
+    dec.set_profiling(True)
+    out = torch.empty(sh.nbytes, dtype=torch.uint8, device=dev)
+    gathered = None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step():
+        dec.decode_blocks(llr, sh.stage0, n_total, sh.block0, sh.nblocks, out=out)
+        if world > 1:
+            return S.gather_bits(out, sh, n_total, D)
+        return out
+
+    # measured ACS roofline of this device (pbvd_probe_acs_peak)
+    peak_acs, _ = P.probe_acs_peak(local)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        gathered = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    times, fwd, tb, launches = [], [], [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            gathered = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            f, t, n = dec.kernel_times()
+            fwd.append(f)
+            tb.append(t)
+            launches += n
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    total_ms = sum(times)
+    tms = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+    total_ms = float(tms.item())
+    ms_per_step = total_ms / args.steps
+    value = n_total / (ms_per_step * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (forward) --------------------------
+    acs_step = acs_per_block_span(n_total, D, L, K, True, sh.block0, sh.nblocks)
+    fwd_ms = statistics.median(fwd)
+    tb_ms = statistics.median(tb)
+    achieved = acs_step / (fwd_ms * 1e-3)
+    R = len(code["polys"])
+    N = 1 << (K - 1)
+    span = D + 2 * L
+    in_bytes = synth.llr_count(R, punct, sh.stage1) - synth.llr_count(R, punct, sh.stage0)
+    nb_rank = sh.nblocks
+    dec_bytes = nb_rank * span * N // 8
+    fwd_hbm_gbs = (in_bytes + dec_bytes) / (fwd_ms * 1e-3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic, _ = load_traffic()
+    roofline = {
+        "bound": "alu", "achieved": achieved / 1e12, "peak": peak_acs / 1e12, "unit": "Tacs/s",
+        "frac": achieved / peak_acs, "traffic": traffic,
+        "kernel": f"fwd_kernel (K={K}, lanes={dec.lanes})",
+        "peak_source": "pbvd_probe_acs_peak: measured minimal 16x2 ACS+decision sequence, "
+                       "all SMs, this run",
+        "acs_per_launch": acs_step, "fwd_ms": fwd_ms, "tb_ms": tb_ms,
+        "fwd_share_of_step": fwd_ms / ms_per_step,
+        "hbm": {"algorithmic_bytes_per_launch": in_bytes + dec_bytes, "achieved_gbs": fwd_hbm_gbs,
+                "peak_gbs": hbm_peak, "frac": fwd_hbm_gbs / hbm_peak,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+    }
+
+    # ---- parity spot check inside the bench (never timed) ------------------
+    parity = None
+    if rank == 0:
+        try:
+            from oracle import oracle as O
+            O.build()
+            nchk = min(sh.nblocks, 64)
+            # first blocks of the rank plus the last ones (edges)
+            blocks = list(range(sh.block0, sh.block0 + nchk // 2)) + \
+                list(range(sh.block0 + sh.nblocks - nchk // 2, sh.block0 + sh.nblocks))
+            llr_h = llr.cpu().numpy()
+            got = np.unpackbits(out.cpu().numpy(), bitorder="little")
+            ok = True
+            for b in sorted(set(blocks)):
+                want = O.decode(code, llr_h, n_total, D, L, punct=punct, b0=b, nblk=1,
+                                window_stage0=sh.stage0, threads=1)
+                t0 = (b - sh.block0) * D
+                ok &= bool((got[t0:t0 + want.size] == want).all())
+            parity = {"blocks_checked": len(set(blocks)), "bit_exact": ok}
+        except Exception as e:  # pragma: no cover
+            parity = {"error": str(e)}
+
+    # ---- end to end through the C ABI with host buffers ---------------------
+    e2e = None
+    if not args.no_e2e:
+        llr_h = llr.cpu().pin_memory()
+        out_h = torch.empty(sh.nbytes, dtype=torch.uint8).pin_memory()
+        dec.decode_host(llr_h, n_total, out=out_h, window_stage0=sh.stage0, block0=sh.block0,
+                        nblocks=sh.nblocks)
+        ts = []
+        for _ in range(args.e2e_steps):
+            if world > 1:
+                dist.barrier()
+            t = time.perf_counter()
+            dec.decode_host(llr_h, n_total, out=out_h, window_stage0=sh.stage0,
+                            block0=sh.block0, nblocks=sh.nblocks)
+            ts.append(time.perf_counter() - t)
+        e2e_s = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        same = bool(torch.equal(out_h, out.cpu()))
+        e2e = {"value": n_total / float(e2e_s.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(llr_h.numel()), "d2h_bytes_per_step": int(out_h.numel()),
+               "api": "pbvd_decode_host (pinned host buffers, 3 streams)",
+               "matches_device_path": same}
+
+    # ---- CPU baseline: the oracle on this host (rank 0, N == 1) ------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        O.build()
+        cpu = cpu_oracle_sample(code, punct, c, llr.cpu().numpy(), n_total, args.cpu_seconds,
+                                ws0=sh.stage0, b_first=sh.block0, max_blocks=sh.nblocks)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "int16",
+            "data": "synthetic (seeded BPSK/AWGN, 8-bit quantised)",
+            "config": {"workload": describe(c, code, n_total, world),
+                       "n_info_total": n_total, "D": D, "L": L, "lanes": dec.lanes,
+                       "l2": "flushed (256 MiB memset) before every timed step",
+                       "parallelism": f"block-range shards x{world}"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(), "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -118,14 +118,19 @@ int pbvd_decode_blocks(pbvd_t h, const int8_t *d_llr_window, int64_t window_stag
                        int64_t window_n_llr, int64_t n_info_total, int64_t block0,
                        int64_t nblocks, uint8_t *d_bits, void *stream);
 
-/* End-to-end decode from HOST memory: copies h_llr to the device, decodes and
- * copies the packed bits back to h_bits, pipelined in segments over
- * `n_streams` internal CUDA streams so transfers overlap the kernels (§IV.C,
- * P:284-301).  h_llr / h_bits should be pinned (cudaHostAlloc /
- * torch pin_memory) for overlap; pageable memory works but serialises.
- * Synchronous: returns when h_bits is complete. */
-int pbvd_decode_host(pbvd_t h, const int8_t *h_llr, int64_t n_llr, uint8_t *h_bits,
-                     int64_t n_info, int n_streams);
+/* End-to-end decode of blocks [block0, block0+nblocks) from HOST memory
+ * (arguments as pbvd_decode_blocks, but h_llr_window / h_bits are host
+ * pointers): the range is cut into segments that are copied to the device,
+ * decoded and copied back on `n_streams` internal CUDA streams (1..8), so the
+ * H2D / D2H transfers of one segment overlap the kernels of another -- the
+ * multi-stream scheme of §IV.C.  For a whole stream pass
+ * window_stage0 = 0, window_n_llr = pbvd_llr_count(n_info), block0 = 0,
+ * nblocks = pbvd_block_count(n_info).  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for overlap; pageable memory works but
+ * serialises.  Synchronous: returns when h_bits is complete. */
+int pbvd_decode_host(pbvd_t h, const int8_t *h_llr_window, int64_t window_stage0,
+                     int64_t window_n_llr, int64_t n_info_total, int64_t block0,
+                     int64_t nblocks, uint8_t *h_bits, int n_streams);
 
 /* Tuning / introspection ------------------------------------------------- */
 
@@ -153,6 +158,13 @@ typedef struct {
     size_t workspace_bytes;      /* currently allocated                    */
 } pbvd_info;
 int pbvd_get_info(pbvd_t h, pbvd_info *info);
+
+/* Diagnostic: the measured ACS roofline of device `device`.  Runs, from
+ * registers only, the minimal 16x2 SIMD instruction sequence that produces a
+ * path metric and a packed survivor bit per state and block (Eq. 1, P:72-74;
+ * P:258) on every SM, and returns ACS per second (one ACS = one state of one
+ * block at one stage) and the best kernel time in ms.  Synchronous. */
+int pbvd_probe_acs_peak(int device, double *acs_per_s, double *ms);
 
 /* Compiled (K, R, polys...) combinations, as text "K:R:o1,o2[,o3]:lanes;..." */
 const char *pbvd_supported(void);

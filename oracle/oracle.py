@@ -55,7 +55,7 @@ def lib():
         L.orc_llr_count.restype = i64
         L.orc_plan.argtypes = [i64, i64, i32, i32, i64, vp, vp, vp, vp]
         L.orc_plan.restype = i64
-        L.orc_decode_range.argtypes = [i32, i32, u32p, i32, vp, vp, i64, i64, i32, i32,
+        L.orc_decode_range.argtypes = [i32, i32, u32p, i32, vp, vp, i64, i64, i64, i32, i32,
                                        ctypes.c_uint, i64, i64, i32, vp, vp, vp]
         L.orc_decode_range.restype = i64
         L.orc_block_decisions.argtypes = [i32, i32, u32p, i32, vp, vp, i64, i64, i32, i32,
@@ -146,11 +146,13 @@ def plan(n_info, n_stages, D, L, b):
 
 
 def decode(code, llr, n_info, D, L, flags=TERMINATED, punct=None, threads=None,
-           b0=0, nblk=None, return_starts=False, return_ties=False):
+           b0=0, nblk=None, return_starts=False, return_ties=False, window_stage0=0):
     """Segmented PBVD decode of blocks [b0, b0+nblk).
 
-    Returns the unpacked decoded bits (uint8 0/1) of those blocks' decoding
-    ranges, plus start states / tie count on request."""
+    `llr` is the whole stream, or (window_stage0 > 0) the soft values from the
+    first kept value of stage window_stage0 on.  Returns the unpacked decoded
+    bits (uint8 0/1) of those blocks' decoding ranges, plus start states / tie
+    count on request."""
     K, polys = code["K"], code["polys"]
     R = len(polys)
     P, pm, pp = _punct(punct, R)
@@ -165,8 +167,8 @@ def decode(code, llr, n_info, D, L, flags=TERMINATED, punct=None, threads=None,
     ties = ctypes.c_int64()
     if threads is None:
         threads = os.cpu_count() or 1
-    rc = lib().orc_decode_range(K, R, _polys(polys), P, pp, ap, n_llr, n_info, D, L, flags,
-                                b0, nblk, threads, bits.ctypes.data, starts.ctypes.data,
+    rc = lib().orc_decode_range(K, R, _polys(polys), P, pp, ap, window_stage0, n_llr, n_info, D,
+                                L, flags, b0, nblk, threads, bits.ctypes.data, starts.ctypes.data,
                                 ctypes.addressof(ties))
     if rc < 0:
         raise ValueError(f"orc_decode_range failed: {rc}")

@@ -105,16 +105,23 @@ int64_t orc_llr_count(int R, int P, const uint8_t *punct, int64_t n_stages) {
     return kept_before(R, P, punct, n_stages);
 }
 
-/* Depuncture the stage range [s0, s1) into lam[(s-s0)*R + r]: the next kept
- * int8 value, or 0 (erasure) at a punctured position (c-18). */
-static void depuncture_range(int R, int P, const uint8_t *punct, const int8_t *llr,
-                             int64_t s0, int64_t s1, int32_t *lam) {
-    int64_t i = kept_before(R, P, punct, s0);
+/* Depuncture stages [s0, s1) reading kept values from llr[i], llr[i+1], ...
+ * (llr[i] being the first kept value of stage s0). */
+static void depuncture_from(int R, int P, const uint8_t *punct, const int8_t *llr, int64_t i,
+                            int64_t s0, int64_t s1, int32_t *lam) {
     for (int64_t s = s0; s < s1; s++)
         for (int r = 0; r < R; r++) {
             int keep = (P <= 1 || !punct) ? 1 : punct[r * P + (int)(s % P)];
             lam[(s - s0) * R + r] = keep ? llr[i++] : 0;
         }
+}
+
+/* Depuncture the stage range [s0, s1) into lam[(s-s0)*R + r]: the next kept
+ * int8 value, or 0 (erasure) at a punctured position (c-18). */
+static void depuncture_range(int R, int P, const uint8_t *punct, const int8_t *llr,
+                             int64_t s0, int64_t s1, int32_t *lam) {
+    int64_t i = kept_before(R, P, punct, s0);
+    depuncture_from(R, P, punct, llr, i, s0, s1, lam);
 }
 
 /* Branch metric, canonical integer form (c-4): BM(c) = sum_r c_r*lam_r,
@@ -152,7 +159,8 @@ typedef struct {
     const uint32_t *polys;
     int P;
     const uint8_t *punct;
-    const int8_t *llr;       /* the punctured stream, [stage][r] (c-17)   */
+    const int8_t *llr;       /* soft values from stage ws0, [stage][r] (c-17) */
+    int64_t kb_ws0;          /* kept values before stage ws0 (index of llr[0]) */
     int64_t n_info, n_stages;
     int D, L;
     unsigned flags;
@@ -176,7 +184,8 @@ static int orc_block(const orc_job *J, int64_t b, uint8_t *dec_out) {
     uint8_t *dec = dec_out ? dec_out : (uint8_t *)malloc((size_t)span * N);
     int *outs = (int *)malloc(sizeof(int) * N * 2);
     if (!lam || !pm || !pmn || !dec || !outs) return -1;
-    depuncture_range(R, J->P, J->punct, J->llr, lo, hi, lam);
+    depuncture_from(R, J->P, J->punct, J->llr,
+                    kept_before(R, J->P, J->punct, lo) - J->kb_ws0, lo, hi, lam);
     for (int d = 0; d < N; d++)
         for (int x = 0; x < 2; x++) outs[d * 2 + x] = orc_out(K, R, J->polys, (uint32_t)d, x);
 
@@ -244,26 +253,35 @@ static int check_code(int K, int R, int D, int L, int64_t n_info) {
 /* Segmented PBVD decode of the blocks [b0, b0+nblk) of a stream:
  * every block decoded independently (static split over `threads` pthreads),
  * outputs gathered in stream order.
- *   llr     : the whole punctured stream, n_llr int8 values, [stage][r]
- *             order, punctured positions omitted (c-17)
+ *   llr     : n_llr int8 soft values of the punctured stream starting at the
+ *             first kept value of stage ws0 ([stage][r] order, punctured
+ *             positions omitted, c-17); ws0 = 0 for a whole stream
  *   n_info  : info bits; n_stages = n_info + (TERMINATED ? K-1 : 0)
  *   bits    : unpacked decoded bits of [t0(b0), t1(b0+nblk-1)), one per byte
  *   starts  : optional, nblk int32 start states
  *   ties    : optional, total exact ACS ties (int64)
  * Returns the total block count of the stream, or a negative value. */
 int64_t orc_decode_range(int K, int R, const uint32_t *polys, int P, const uint8_t *punct,
-                         const int8_t *llr, int64_t n_llr, int64_t n_info, int D, int L,
-                         unsigned flags, int64_t b0, int64_t nblk, int threads,
+                         const int8_t *llr, int64_t ws0, int64_t n_llr, int64_t n_info, int D,
+                         int L, unsigned flags, int64_t b0, int64_t nblk, int threads,
                          uint8_t *bits, int32_t *starts, int64_t *ties_total) {
     if (check_code(K, R, D, L, n_info)) return -1;
     int64_t n_stages = n_info + ((flags & ORC_TERMINATED) ? K - 1 : 0);
-    if (orc_llr_count(R, P, punct, n_stages) != n_llr) return -3;
     int64_t nb = (n_info + D - 1) / D;
-    if (b0 < 0 || nblk < 1 || b0 + nblk > nb) return -1;
+    if (b0 < 0 || nblk < 1 || b0 + nblk > nb || ws0 < 0) return -1;
+    /* the window [ws0, ...) must hold every span of the range */
+    int64_t kb_ws0 = kept_before(R, P, punct, ws0);
+    {
+        int64_t t0, t1, lo, hi, u0, u1, ulo, uhi;
+        orc_plan(n_info, n_stages, D, L, b0, &t0, &t1, &lo, &hi);
+        orc_plan(n_info, n_stages, D, L, b0 + nblk - 1, &u0, &u1, &ulo, &uhi);
+        if (lo < ws0 || kept_before(R, P, punct, uhi) - kb_ws0 > n_llr) return -3;
+    }
     int32_t *st = (int32_t *)malloc(sizeof(int32_t) * (size_t)nblk);
     int64_t *tie = (int64_t *)calloc((size_t)nblk, sizeof(int64_t));
     if (!st || !tie) return -2;
-    orc_job J = {K, R, polys, P, punct, llr, n_info, n_stages, D, L, flags, b0, bits, st, tie};
+    orc_job J = {K, R, polys, P, punct, llr, kb_ws0, n_info, n_stages, D, L, flags, b0, bits, st,
+                 tie};
     if (threads < 1) threads = 1;
     if (threads > nblk) threads = (int)nblk;
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * threads);
@@ -303,7 +321,7 @@ int orc_block_decisions(int K, int R, const uint32_t *polys, int P, const uint8_
     uint8_t *bits = (uint8_t *)calloc((size_t)(t1 - t0), 1);
     int32_t st = 0;
     int64_t tie = 0;
-    orc_job J = {K, R, polys, P, punct, llr, n_info, n_stages, D, L, flags, b, bits, &st, &tie};
+    orc_job J = {K, R, polys, P, punct, llr, 0, n_info, n_stages, D, L, flags, b, bits, &st, &tie};
     int rc = orc_block(&J, b, dec);
     *lo_out = lo; *hi_out = hi; *start = st;
     free(bits);

@@ -16,7 +16,7 @@ EXPORTS = (
     "pbvd_create", "pbvd_destroy", "pbvd_llr_count", "pbvd_stage_count", "pbvd_block_count",
     "pbvd_decode", "pbvd_decode_blocks", "pbvd_decode_host", "pbvd_set_lanes", "pbvd_get_lanes",
     "pbvd_set_workspace_limit", "pbvd_set_profiling", "pbvd_kernel_times", "pbvd_get_info",
-    "pbvd_supported", "pbvd_strerror", "pbvd_last_error",
+    "pbvd_supported", "pbvd_strerror", "pbvd_last_error", "pbvd_probe_acs_peak",
 )
 
 
@@ -55,7 +55,7 @@ def load(path: os.PathLike | None = None):
     L.pbvd_decode.restype = i32
     L.pbvd_decode_blocks.argtypes = [h, vp, i64, i64, i64, i64, i64, vp, vp]
     L.pbvd_decode_blocks.restype = i32
-    L.pbvd_decode_host.argtypes = [h, vp, i64, vp, i64, i32]
+    L.pbvd_decode_host.argtypes = [h, vp, i64, i64, i64, i64, i64, vp, i32]
     L.pbvd_decode_host.restype = i32
     L.pbvd_set_lanes.argtypes = [h, i32]
     L.pbvd_set_lanes.restype = i32
@@ -70,6 +70,9 @@ def load(path: os.PathLike | None = None):
     L.pbvd_kernel_times.restype = i32
     L.pbvd_get_info.argtypes = [h, ctypes.POINTER(PbvdInfo)]
     L.pbvd_get_info.restype = i32
+    L.pbvd_probe_acs_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_double)]
+    L.pbvd_probe_acs_peak.restype = i32
     L.pbvd_supported.argtypes = []
     L.pbvd_supported.restype = cp
     L.pbvd_strerror.argtypes = [i32]

@@ -218,13 +218,13 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const uint2 lw,
             const int a = CF::alpha_reg(k, P);
             const uint32_t E = pm[k], O = pm[k | pb];
             // x = 0: min(E + BM(alpha), O + BM(gamma))        (Eqs. 3, 5)
-            const uint32_t mO0 = O + Pv[a ^ g0];
+            const uint32_t mO0 = add32(O, Pv[a ^ g0]);
             const uint32_t nE = __viaddmin_s16x2(E, Pv[a], mO0);
-            const uint32_t tE = E - mO0 + PC[a];
+            const uint32_t tE = sub_add(E, mO0, PC[a]);
             // x = 1: min(E + BM(beta), O + BM(theta))         (Eqs. 4, 6)
-            const uint32_t mO1 = O + Pv[a ^ gK ^ g0];
+            const uint32_t mO1 = add32(O, Pv[a ^ gK ^ g0]);
             const uint32_t nO = __viaddmin_s16x2(E, Pv[a ^ gK], mO1);
-            const uint32_t tO = E - mO1 + PC[a ^ gK];
+            const uint32_t tO = sub_add(E, mO1, PC[a ^ gK]);
             pm[k] = nE;
             pm[k | pb] = nO;
             t[k] = tE;
@@ -257,9 +257,9 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const uint2 lw,
         for (int k = 0; k < S; ++k) {
             const int a = CF::alpha_reg(k, P);
             const uint32_t own = pm[k];
-            const uint32_t mR = recv[k] + Pr[a];
+            const uint32_t mR = add32(recv[k], Pr[a]);
             pm[k] = __viaddmin_s16x2(own, Po[a], mR);
-            t[k] = own - mR + PCo[a];
+            t[k] = sub_add(own, mR, PCo[a]);
         }
         pack_store<CF>(t, 0u - lb, drow);
     }
@@ -280,6 +280,17 @@ __device__ __forceinline__ void cycle(uint32_t (&pm)[CF::S], const uint2* lamrow
                                       const int (&flip)[CF::V], int lg, uint32_t* drow, int s0,
                                       int nst, std::integer_sequence<int, Ps...>) {
     (stage_guarded<CF, Ps>(pm, lamrow, flip, lg, drow, s0 + Ps, nst), ...);
+}
+
+// v stages without guards: one basic block, so the scheduler can overlap the
+// branch-metric chain of stage s+1 with the butterflies of stage s.
+template <class CF, int... Ps>
+__device__ __forceinline__ void cycle_full(uint32_t (&pm)[CF::S], const uint2* lamrow,
+                                           const int (&flip)[CF::V], int lg, uint32_t* drow,
+                                           std::integer_sequence<int, Ps...>) {
+    uint2 lw[sizeof...(Ps)];
+    ((lw[Ps] = lamrow[size_t(Ps) * CF::PPC]), ...);
+    (acs_stage<CF, Ps>(pm, lw[Ps], flip[Ps], lg, drow + size_t(Ps) * CF::ROW), ...);
 }
 
 template <class CF, int... Ps>
@@ -412,9 +423,16 @@ __global__ void __launch_bounds__(CF::NT) fwd_kernel(const __grid_constant__ Fwd
             __syncwarp();
         }
         const int nst = min(T, span - c * T);
+        if (nst == T) {
 #pragma unroll 1
-        for (int s0 = 0; s0 < nst; s0 += V)
-            cycle<CF>(pm, lamrow, flip, lg, drow, s0, nst, std::make_integer_sequence<int, V>{});
+            for (int s0 = 0; s0 < T; s0 += V)
+                cycle_full<CF>(pm, lamrow + size_t(s0) * CF::PPC, flip, lg,
+                               drow + size_t(s0) * ROW, std::make_integer_sequence<int, V>{});
+        } else {
+#pragma unroll 1
+            for (int s0 = 0; s0 < nst; s0 += V)
+                cycle<CF>(pm, lamrow, flip, lg, drow, s0, nst, std::make_integer_sequence<int, V>{});
+        }
         // renormalise: subtract the block minimum (per 16-bit half = per block)
         uint32_t mn = pm[0];
 #pragma unroll

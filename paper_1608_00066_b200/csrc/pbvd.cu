@@ -38,6 +38,22 @@ static std::vector<int> g_prepared;  // per (device, variant) flag
 
 using namespace pbvd;
 
+struct Workspace {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+// Resources of the host-buffer pipeline (pbvd_decode_host): per stream a
+// survivor workspace and device staging buffers for the soft window / bits.
+struct HostLane {
+    cudaStream_t stream = nullptr;
+    Workspace ws;
+    int8_t* d_llr = nullptr;
+    size_t llr_cap = 0;
+    uint8_t* d_bits = nullptr;
+    size_t bits_cap = 0;
+};
+
 struct pbvd_s {
     int device = 0;
     int K = 0, R = 0, V = 0, N = 0;
@@ -49,9 +65,9 @@ struct pbvd_s {
     int D = 0, L = 0, soft_bits = 8;
     unsigned flags = 0;
     const Variant* var = nullptr;
-    void* ws = nullptr;
-    size_t ws_bytes = 0;
+    Workspace ws;
     size_t ws_limit = size_t(4) << 30;
+    std::vector<HostLane> lanes;
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_fwd, ev_tb;   // indices into ev_pool
@@ -101,19 +117,19 @@ int ensure_prepared(pbvd_t h, const Variant* v) {
     return PBVD_OK;
 }
 
-int ensure_ws(pbvd_t h, size_t bytes) {
-    if (h->ws_bytes >= bytes) return PBVD_OK;
-    if (h->ws) {
-        cudaFree(h->ws);   // synchronises the device: no pending kernel uses it
-        h->ws = nullptr;
-        h->ws_bytes = 0;
+int ensure_buf(pbvd_t h, void** p, size_t* cap, size_t bytes) {
+    if (*cap >= bytes) return PBVD_OK;
+    if (*p) {
+        cudaFree(*p);   // synchronises the device: no pending kernel uses it
+        *p = nullptr;
+        *cap = 0;
     }
-    cudaError_t e = cudaMalloc(&h->ws, bytes);
+    cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        return fail(h, PBVD_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
+        return fail(h, PBVD_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     }
-    h->ws_bytes = bytes;
+    *cap = bytes;
     return PBVD_OK;
 }
 
@@ -142,8 +158,8 @@ BlockGeo geo(const pbvd_s* h, int64_t n_info, int64_t n_stages, int64_t nb, int6
     return g;
 }
 
-int run_blocks(pbvd_t h, const int8_t* llr, int64_t ws0, int64_t n_llr_win, int64_t n_info,
-               int64_t B0, int64_t nblk, uint8_t* out, cudaStream_t stream) {
+int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n_llr_win,
+               int64_t n_info, int64_t B0, int64_t nblk, uint8_t* out, cudaStream_t stream) {
     const Variant* v = h->var;
     const int64_t n_stages = n_info + ((h->flags & PBVD_TERMINATED) ? h->V : 0);
     const int64_t nb = (n_info + h->D - 1) / h->D;
@@ -203,9 +219,9 @@ int run_blocks(pbvd_t h, const int8_t* llr, int64_t ws0, int64_t n_llr_win, int6
     const size_t start_bytes = size_t(wave + 64) * 4;
     const size_t need = ((int_bytes + 255) & ~size_t(255)) + ((edge_bytes + 255) & ~size_t(255)) +
                         ((start_bytes + 255) & ~size_t(255));
-    rc = ensure_ws(h, need);
+    rc = ensure_buf(h, &W.p, &W.bytes, need);
     if (rc) return rc;
-    uint8_t* wsb = static_cast<uint8_t*>(h->ws);
+    uint8_t* wsb = static_cast<uint8_t*>(W.p);
     uint32_t* dec_int = reinterpret_cast<uint32_t*>(wsb);
     uint32_t* dec_edge = reinterpret_cast<uint32_t*>(wsb + ((int_bytes + 255) & ~size_t(255)));
     int32_t* start_edge = reinterpret_cast<int32_t*>(
@@ -359,7 +375,13 @@ void pbvd_destroy(pbvd_t h) {
     if (!h) return;
     {
         DeviceGuard g(h->device);
-        if (h->ws) cudaFree(h->ws);
+        if (h->ws.p) cudaFree(h->ws.p);
+        for (auto& ln : h->lanes) {
+            if (ln.ws.p) cudaFree(ln.ws.p);
+            if (ln.d_llr) cudaFree(ln.d_llr);
+            if (ln.d_bits) cudaFree(ln.d_bits);
+            if (ln.stream) cudaStreamDestroy(ln.stream);
+        }
         for (auto ev : h->ev_pool) cudaEventDestroy(ev);
     }
     delete h;
@@ -390,8 +412,8 @@ int pbvd_decode_blocks(pbvd_t h, const int8_t* d_llr_window, int64_t window_stag
     h->ev_fwd.clear();
     h->ev_tb.clear();
     h->launches = 0;
-    return run_blocks(h, d_llr_window, window_stage0, window_n_llr, n_info_total, block0, nblocks,
-                      d_bits, static_cast<cudaStream_t>(stream));
+    return run_blocks(h, h->ws, d_llr_window, window_stage0, window_n_llr, n_info_total, block0,
+                      nblocks, d_bits, static_cast<cudaStream_t>(stream));
 }
 
 int pbvd_decode(pbvd_t h, const int8_t* d_llr, int64_t n_llr, uint8_t* d_bits, int64_t n_info,
@@ -404,39 +426,76 @@ int pbvd_decode(pbvd_t h, const int8_t* d_llr, int64_t n_llr, uint8_t* d_bits, i
                               stream);
 }
 
-int pbvd_decode_host(pbvd_t h, const int8_t* h_llr, int64_t n_llr, uint8_t* h_bits,
-                     int64_t n_info, int n_streams) {
+int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0,
+                     int64_t window_n_llr, int64_t n_info_total, int64_t block0, int64_t nblocks,
+                     uint8_t* h_bits, int n_streams) {
     if (!h) return PBVD_EINVAL;
-    if (!h_llr || !h_bits || n_info < 1) return fail(h, PBVD_EINVAL, "null pointer or empty stream");
-    if (n_llr != pbvd_llr_count(h, n_info))
-        return fail(h, PBVD_ESIZE, "n_llr != pbvd_llr_count(n_info)");
-    (void)n_streams;
+    if (!h_llr_window || !h_bits || n_info_total < 1 || window_n_llr < 1)
+        return fail(h, PBVD_EINVAL, "null pointer or empty stream");
+    const int64_t n_stages = n_info_total + ((h->flags & PBVD_TERMINATED) ? h->V : 0);
+    const int64_t nb = (n_info_total + h->D - 1) / h->D;
+    if (block0 < 0 || nblocks < 1 || block0 + nblocks > nb)
+        return fail(h, PBVD_EINVAL, "block range outside the stream");
+    if (n_streams < 1) n_streams = 1;
+    if (n_streams > 8) n_streams = 8;
     DeviceGuard g(h->device);
-    const size_t out_bytes = size_t((n_info + 7) / 8);
-    int8_t* d_llr = nullptr;
-    uint8_t* d_bits = nullptr;
-    cudaError_t e = cudaMalloc(&d_llr, size_t(n_llr));
-    if (e != cudaSuccess) return cuda_fail(h, e, "cudaMalloc");
-    e = cudaMalloc(&d_bits, out_bytes);
-    if (e != cudaSuccess) {
-        cudaFree(d_llr);
-        return cuda_fail(h, e, "cudaMalloc");
+    h->ev_fwd.clear();
+    h->ev_tb.clear();
+    h->launches = 0;
+    const bool prof = h->prof;
+    h->prof = false;                       // events are per caller stream only
+    const int64_t kb0 = kept_before_h(h, window_stage0);
+    // segments: enough of them to overlap copies with kernels, each large
+    // enough to keep the GPU busy on its own
+    const int64_t min_seg = 8192;
+    int64_t nseg = std::max<int64_t>(1, std::min<int64_t>(2 * n_streams, nblocks / min_seg));
+    const int64_t seg = (nblocks + nseg - 1) / nseg;
+    nseg = (nblocks + seg - 1) / seg;
+    while (int(h->lanes.size()) < n_streams) {
+        HostLane ln;
+        if (cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking) != cudaSuccess) {
+            h->prof = prof;
+            return cuda_fail(h, cudaGetLastError(), "cudaStreamCreate");
+        }
+        h->lanes.push_back(ln);
     }
-    cudaStream_t s;
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     int rc = PBVD_OK;
-    e = cudaMemcpyAsync(d_llr, h_llr, size_t(n_llr), cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemcpyAsync H2D");
-    if (!rc) rc = pbvd_decode(h, d_llr, n_llr, d_bits, n_info, s);
-    if (!rc) {
-        e = cudaMemcpyAsync(h_bits, d_bits, out_bytes, cudaMemcpyDeviceToHost, s);
+    const int64_t bit_base = block0 * h->D;
+    for (int64_t k = 0; k < nseg && rc == PBVD_OK; ++k) {
+        HostLane& ln = h->lanes[size_t(k % n_streams)];
+        const int64_t b0 = block0 + k * seg;
+        const int64_t b1 = std::min(block0 + nblocks, b0 + seg);
+        const BlockGeo ga = geo(h, n_info_total, n_stages, nb, b0);
+        const BlockGeo gz = geo(h, n_info_total, n_stages, nb, b1 - 1);
+        const int64_t k0 = kept_before_h(h, ga.lo), k1 = kept_before_h(h, gz.hi);
+        if (ga.lo < window_stage0 || k1 - kb0 > window_n_llr) {
+            rc = fail(h, PBVD_ESIZE, "soft-value window does not cover the blocks' spans");
+            break;
+        }
+        const size_t nllr = size_t(k1 - k0);
+        const int64_t t0 = b0 * h->D, t1 = std::min<int64_t>(b1 * h->D, n_info_total);
+        const size_t nbytes = size_t((t1 - t0 + 7) / 8);
+        rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_llr), &ln.llr_cap, nllr);
+        if (!rc) rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_bits), &ln.bits_cap, nbytes);
+        if (rc) break;
+        cudaError_t e = cudaMemcpyAsync(ln.d_llr, h_llr_window + (k0 - kb0), nllr,
+                                        cudaMemcpyHostToDevice, ln.stream);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(h, e, "cudaMemcpyAsync H2D");
+            break;
+        }
+        rc = run_blocks(h, ln.ws, ln.d_llr, ga.lo, int64_t(nllr), n_info_total, b0, b1 - b0,
+                        ln.d_bits, ln.stream);
+        if (rc) break;
+        e = cudaMemcpyAsync(h_bits + (t0 - bit_base) / 8, ln.d_bits, nbytes,
+                            cudaMemcpyDeviceToHost, ln.stream);
         if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemcpyAsync D2H");
     }
-    e = cudaStreamSynchronize(s);
-    if (!rc && e != cudaSuccess) rc = cuda_fail(h, e, "decode");
-    cudaStreamDestroy(s);
-    cudaFree(d_llr);
-    cudaFree(d_bits);
+    for (int i = 0; i < n_streams; ++i) {
+        cudaError_t e = cudaStreamSynchronize(h->lanes[size_t(i)].stream);
+        if (!rc && e != cudaSuccess) rc = cuda_fail(h, e, "decode (host pipeline)");
+    }
+    h->prof = prof;
     return rc;
 }
 
@@ -502,7 +561,8 @@ int pbvd_get_info(pbvd_t h, pbvd_info* info) {
     info->P = h->P;
     info->span = h->D + 2 * h->L;
     info->dec_bytes_per_block = int64_t(h->D + 2 * h->L) * (h->N / 8 > 0 ? h->N / 8 : 1);
-    info->workspace_bytes = h->ws_bytes;
+    info->workspace_bytes = h->ws.bytes;
+    for (const auto& ln : h->lanes) info->workspace_bytes += ln.ws.bytes;
     return PBVD_OK;
 }
 

@@ -16,6 +16,21 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return d;
 }
 
+// a - b + c as one IADD3; opaque to NVVM so it cannot re-associate the
+// decision computation across butterflies (which costs extra instructions).
+__device__ __forceinline__ uint32_t sub_add(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("{.reg .u32 t;\n\tsub.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;}"
+        : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+// a + b (plain 32-bit add; exact 16x2 add for non-negative halves)
+__device__ __forceinline__ uint32_t add32(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("add.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
 // ---- Ampere-style 16-byte async copy global -> shared (LDGSTS) ------------
 __device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");

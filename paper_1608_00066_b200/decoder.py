@@ -33,6 +33,15 @@ def supported():
     return out
 
 
+def probe_acs_peak(device: int = 0):
+    """pbvd_probe_acs_peak: (measured ACS/s roofline, kernel ms)."""
+    L = _lib.load()
+    a, m = ctypes.c_double(), ctypes.c_double()
+    _check(L.pbvd_probe_acs_peak(int(device), ctypes.byref(a), ctypes.byref(m)), None,
+           "pbvd_probe_acs_peak")
+    return a.value, m.value
+
+
 class Decoder:
     """pbvd_create(...) -- see include/pbvd.h for the meaning of every argument.
 
@@ -109,15 +118,23 @@ class Decoder:
         return out
 
     def decode_host(self, llr: torch.Tensor, n_info: int, out: torch.Tensor | None = None,
-                    n_streams: int = 3) -> torch.Tensor:
-        """pbvd_decode_host: host int8 tensor (pinned for overlap) -> host packed bits."""
+                    n_streams: int = 3, window_stage0: int = 0, block0: int = 0,
+                    nblocks: int | None = None) -> torch.Tensor:
+        """pbvd_decode_host: host int8 window (pinned for overlap) -> host packed bits.
+
+        Defaults decode the whole stream; a shard passes its window and range."""
         if llr.dtype != torch.int8 or llr.is_cuda or not llr.is_contiguous():
             raise ValueError("llr must be a contiguous int8 CPU tensor")
-        nbytes = (int(n_info) + 7) // 8
+        if nblocks is None:
+            nblocks = self.block_count(n_info) - int(block0)
+        t0 = int(block0) * self.D
+        t1 = min((int(block0) + int(nblocks)) * self.D, int(n_info))
+        nbytes = (t1 - t0 + 7) // 8
         if out is None:
             out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=llr.is_pinned())
-        rc = self._L.pbvd_decode_host(self._h, llr.data_ptr(), llr.numel(), out.data_ptr(),
-                                      int(n_info), int(n_streams))
+        rc = self._L.pbvd_decode_host(self._h, llr.data_ptr(), int(window_stage0), llr.numel(),
+                                      int(n_info), int(block0), int(nblocks), out.data_ptr(),
+                                      int(n_streams))
         _check(rc, self._h, "pbvd_decode_host")
         return out
 

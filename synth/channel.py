@@ -135,15 +135,10 @@ def encode(x_ext: torch.Tensor, K: int, polys) -> torch.Tensor:
     return out
 
 
-def make_window(code, n_info, ebn0_db, seed, s0, s1, punct=None, hard=False, terminated=True,
-                device="cpu", frac_bits=5):
-    """int8 soft values of stages [s0, s1) of the stream (kept positions only),
-    i.e. exactly llr[llr_count(s0) : llr_count(s1)] of the whole stream."""
+def _piece(code, n_info, sigma, seed, s0, s1, punct, hard, device, frac_bits, cs, ce):
+    """Soft values of stages [s0, s1) inside noise chunk [cs, ce)."""
     K, polys = code["K"], code["polys"]
     R, v = len(polys), K - 1
-    n_stages = n_stages_of(code, n_info, terminated)
-    assert 0 <= s0 <= s1 <= n_stages
-    # encoder input for stages [s0 - v, s1): info bits, zero before 0 / in the tail
     a, b = max(0, s0 - v), min(n_info, s1)
     x = torch.zeros(s1 - s0 + v, dtype=torch.uint8, device=device)
     if b > a:
@@ -153,31 +148,43 @@ def make_window(code, n_info, ebn0_db, seed, s0, s1, punct=None, hard=False, ter
     keep = _keep(punct, R)
     if keep is not None:
         P = keep.shape[1]
-        cols = (torch.arange(s0, s1, device=device) % P)
-        mask = keep.to(device)[:, cols].t().bool()               # [s1-s0, R]
-        sym = sym[mask]
+        cols = torch.arange(s0, s1, device=device) % P
+        sym = sym[keep.to(device)[:, cols].t().bool()]
     else:
         sym = sym.reshape(-1)
-    # noise: per 2^20-stage chunk, one draw per kept value of the chunk
-    sigma = sigma_for(ebn0_db, code_rate(code, punct))
-    noise = torch.empty_like(sym)
-    pos = 0
-    c0 = s0 // NOISE_CHUNK
-    c1 = (s1 - 1) // NOISE_CHUNK if s1 > s0 else c0 - 1
-    for c in range(c0, c1 + 1):
-        cs, ce = c * NOISE_CHUNK, min((c + 1) * NOISE_CHUNK, n_stages)
-        k0, k1 = llr_count(R, punct, cs), llr_count(R, punct, ce)
-        z = torch.randn(k1 - k0, generator=_gen(device, seed, c, 23), device=device)
-        lo = llr_count(R, punct, max(s0, cs)) - k0
-        hi = llr_count(R, punct, min(s1, ce)) - k0
-        noise[pos:pos + hi - lo] = z[lo:hi]
-        pos += hi - lo
-    y = sym + sigma * noise
+    k0, k1 = llr_count(R, punct, cs), llr_count(R, punct, ce)
+    c = cs // NOISE_CHUNK
+    z = torch.randn(k1 - k0, generator=_gen(device, seed, c, 23), device=device)
+    lo = llr_count(R, punct, s0) - k0
+    y = sym + sigma * z[lo:lo + sym.numel()]
     if hard:
-        llr = torch.where(y >= 0, 1, -1).to(torch.int8)
-    else:
-        llr = torch.clamp(torch.round(y * (1 << frac_bits)), -127, 127).to(torch.int8)
-    return llr
+        return torch.where(y >= 0, 1, -1).to(torch.int8)
+    return torch.clamp(torch.round(y * (1 << frac_bits)), -127, 127).to(torch.int8)
+
+
+def make_window(code, n_info, ebn0_db, seed, s0, s1, punct=None, hard=False, terminated=True,
+                device="cpu", frac_bits=5, out=None):
+    """int8 soft values of stages [s0, s1) of the stream (kept positions only),
+    i.e. exactly llr[llr_count(s0) : llr_count(s1)] of the whole stream.
+    Generated piecewise (one noise chunk at a time) so any size fits."""
+    R = len(code["polys"])
+    n_stages = n_stages_of(code, n_info, terminated)
+    assert 0 <= s0 <= s1 <= n_stages
+    sigma = sigma_for(ebn0_db, code_rate(code, punct))
+    n = llr_count(R, punct, s1) - llr_count(R, punct, s0)
+    if out is None:
+        out = torch.empty(n, dtype=torch.int8, device=device)
+    assert out.numel() == n
+    base = llr_count(R, punct, s0)
+    for c in range(s0 // NOISE_CHUNK, (s1 - 1) // NOISE_CHUNK + 1 if s1 > s0 else 0):
+        cs, ce = c * NOISE_CHUNK, min((c + 1) * NOISE_CHUNK, n_stages)
+        a, b = max(s0, cs), min(s1, ce)
+        if b <= a:
+            continue
+        piece = _piece(code, n_info, sigma, seed, a, b, punct, hard, device, frac_bits, cs, ce)
+        i = llr_count(R, punct, a) - base
+        out[i:i + piece.numel()] = piece
+    return out
 
 
 def make_stream(code, n_info, ebn0_db, seed, punct=None, hard=False, terminated=True,
