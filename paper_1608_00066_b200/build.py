@@ -20,7 +20,7 @@ LIB = PKG / "libpbvd.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
-         f"-I{ROOT / 'include'}"]
+         f"-I{ROOT / 'include'}"] + os.environ.get("PBVD_NVCC_EXTRA", "").split()
 
 
 def _sources():

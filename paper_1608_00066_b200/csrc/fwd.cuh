@@ -33,11 +33,15 @@
 //     8 such words merged by LOP3 into one 32-bit word (32 decisions), stored
 //     to shared memory; each warp streams T stages of survivors to HBM with
 //     one cp.async.bulk (TMA engine) per chunk.
-//   * soft inputs: 16-byte cp.async (LDGSTS) of each block's window into
-//     shared memory (double buffered), depunctured per block into a
-//     [stage][pair] table read with one 8-byte LDS per stage per lane.
+//   * every warp is an autonomous pipeline (no CTA barrier anywhere): it
+//     copies its blocks' soft windows of the NEXT chunk with 16-byte cp.async
+//     (LDGSTS) while it computes the current one, then depunctures them into
+//     per-stage, per-pair packed 16x2 operands x_r = max(lam_r,0),
+//     y_r = max(-lam_r,0) in shared memory, read with one 16/32-byte LDS per
+//     stage one stage ahead of use.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <utility>
 #include "params.h"
 #include "ptx.cuh"
@@ -74,17 +78,27 @@ struct Cfg {
     static constexpr int WPS = S >= 16 ? S / 16 : 1;   // decision words per lane per stage
     static constexpr int PPW = 32 / W_;       // block pairs per warp
     static constexpr int BPW = 2 * PPW;       // blocks per warp (= per survivor region)
-    static constexpr int NWARP = cmax(1, cmin(8, (N >= 256 ? 64 : 128) / BPW));
+    static constexpr int NWARP = 1;            // warps per CTA (each warp is autonomous)
     static constexpr int NT = NWARP * 32;
+    static constexpr int MAXREG = 200;         // room for the unrolled stage state
     static constexpr int BPC = NWARP * BPW;   // blocks per CTA
     static constexpr int PPC = NWARP * PPW;   // pairs per CTA
     static constexpr int T = V * (32 / V);    // stages per chunk = normalisation period
-    static constexpr int RAWB = ((T * R + 15) / 16) * 16 + 32;   // raw window bytes
+    // raw window per block and chunk: the T*R soft bytes rounded out to
+    // 16-byte vectors; an odd number of 16-byte vectors per window keeps both
+    // the cp.async writes and the transform's byte reads bank-conflict free
+    static constexpr int BOXB = ((T * R + 15) / 16) * 16 + 16;
+    static constexpr int RAWB = ((BOXB / 16) & 1) ? BOXB : BOXB + 16;
     static constexpr int ROW = 32 * WPS;      // survivor words per stage per region
-    static constexpr size_t SMEM_RAW = size_t(2) * BPC * RAWB;
-    static constexpr size_t SMEM_LAM = size_t(T) * PPC * 8;
-    static constexpr size_t SMEM_DEC = size_t(NWARP) * T * ROW * 4;
-    static constexpr size_t SMEM = SMEM_RAW + SMEM_LAM + SMEM_DEC;
+    static constexpr int XYW = (R == 2) ? 4 : 8;   // packed x/y words per pair-stage
+    // per warp: raw windows [BPW][RAWB], operands [T][PPW][XYW], survivors [T][32][WPS]
+    static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
+    static constexpr int SLICE = (PPW + NCYC - 1) / NCYC;  // pairs transformed per cycle
+    static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
+    static constexpr size_t WLAM = size_t(2) * T * PPW * XYW * 4;  // double buffered
+    static constexpr size_t WDEC = size_t(T) * ROW * 4;
+    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEC + 127) / 128) * 128;
+    static constexpr size_t SMEM = NWARP * WSMEM;
 
     // alpha of the butterfly whose E slot has register index k, restricted
     // to the register bits (Eq. 3 on the physical->logical bit map of phase p)
@@ -118,21 +132,36 @@ __device__ __forceinline__ int lane_alpha(int lg) {
     return a;
 }
 
+// x/y operands of one stage for a block pair: xy[2r] = x_r, xy[2r+1] = y_r
+template <class CF>
+struct XY {
+    uint32_t v[CF::XYW];
+};
+
+template <class CF>
+__device__ __forceinline__ XY<CF> load_xy(const uint32_t* lamrow, int s) {
+    XY<CF> r;
+    const uint4* q = reinterpret_cast<const uint4*>(lamrow + size_t(s) * CF::PPW * CF::XYW);
+    const uint4 a = q[0];
+    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+    if constexpr (CF::XYW == 8) {
+        const uint4 b = q[1];
+        r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+    }
+    return r;
+}
+
 // The 2^R non-negative codeword metrics of one stage for a block pair,
-// permuted by the lane's alpha offset: Pv[c] = BM+(c ^ flip).
+// permuted by the lane's alpha offset: Pv[c] = BM+(c ^ flip), where
 //   BM+(c) = sum_r (c_r ? max(lam_r,0) : max(-lam_r,0))   (c-4, canonical + const)
 template <class CF, int POSS>
-__device__ __forceinline__ void bm_vector(const uint2 lw, int flip, uint32_t (&Pv)[CF::NC]) {
+__device__ __forceinline__ void bm_vector(const XY<CF>& xy, int flip, uint32_t (&Pv)[CF::NC]) {
     constexpr int R = CF::R;
     uint32_t x[R], y[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        // (lam_A_r, lam_B_r) sign-extended to 16x2
-        const uint32_t sel = uint32_t(r) | (uint32_t(8 | r) << 4) | (uint32_t(4 + r) << 8) |
-                             (uint32_t(12 + r) << 12);
-        const uint32_t l = prmt(lw.x, lw.y, sel);
-        x[r] = __vmaxs2(l, 0u);
-        y[r] = __vsub2(x[r], l);
+        x[r] = xy.v[2 * r];
+        y[r] = xy.v[2 * r + 1];
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -147,7 +176,7 @@ __device__ __forceinline__ void bm_vector(const uint2 lw, int flip, uint32_t (&P
     for (int c = 0; c < CF::NC; ++c) {
         uint32_t s = ((c & 1) ? x[0] : y[0]);
 #pragma unroll
-        for (int r = 1; r < R; ++r) s += ((c >> r) & 1) ? x[r] : y[r];
+        for (int r = 1; r < R; ++r) s = add32(s, ((c >> r) & 1) ? x[r] : y[r]);
         Pv[c] = s;
     }
 }
@@ -199,7 +228,7 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
 
 // One trellis stage at compile-time phase P (Eq. 1 per output state).
 template <class CF, int P>
-__device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const uint2 lw, int flip,
+__device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
                                           int lg, uint32_t* drow) {
     using C = typename CF::code;
     constexpr int S = CF::S, NC = CF::NC;
@@ -208,9 +237,9 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const uint2 lw,
     if constexpr (P < CF::LB) {
         // ---- butterfly partner in this lane (register bit P) --------------
         uint32_t Pv[NC], PC[NC];
-        bm_vector<CF, CF::lane_possible(P)>(lw, flip, Pv);
+        bm_vector<CF, CF::lane_possible(P)>(xy, flip, Pv);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) PC[c] = Pv[c] + 0x7FFF7FFFu;
+        for (int c = 0; c < NC; ++c) PC[c] = add32(Pv[c], 0x7FFF7FFFu);
         constexpr int pb = 1 << P;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -242,17 +271,17 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const uint2 lw,
         const uint32_t Cc = 0x7FFF7FFFu + lb * 0x00010001u;   // inverted sense on O side
         if constexpr (C::symmetric) {
             // own: alpha (E side) / theta = alpha (O side); other: gamma = beta = ~alpha
-            bm_vector<CF, CF::lane_possible(P)>(lw, flip, Po);
+            bm_vector<CF, CF::lane_possible(P)>(xy, flip, Po);
 #pragma unroll
             for (int c = 0; c < NC; ++c) Pr[c] = Po[c ^ C::ALL];
         } else {
             const int fo = flip ^ (lb ? (gK ^ g0) : 0);
             const int fr = flip ^ (lb ? gK : g0);
-            bm_vector<CF, CF::lane_possible(P) | (gK ^ g0)>(lw, fo, Po);
-            bm_vector<CF, CF::lane_possible(P) | gK | g0>(lw, fr, Pr);
+            bm_vector<CF, CF::lane_possible(P) | (gK ^ g0)>(xy, fo, Po);
+            bm_vector<CF, CF::lane_possible(P) | gK | g0>(xy, fr, Pr);
         }
 #pragma unroll
-        for (int c = 0; c < NC; ++c) PCo[c] = Po[c] + Cc;
+        for (int c = 0; c < NC; ++c) PCo[c] = add32(Po[c], Cc);
 #pragma unroll
         for (int k = 0; k < S; ++k) {
             const int a = CF::alpha_reg(k, P);
@@ -265,33 +294,27 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const uint2 lw,
     }
 }
 
-template <class CF, int P>
-__device__ __forceinline__ void stage_guarded(uint32_t (&pm)[CF::S], const uint2* lamrow,
-                                              const int (&flip)[CF::V], int lg,
-                                              uint32_t* drow, int s, int nst) {
-    if (s < nst) {
-        const uint2 lw = lamrow[size_t(s) * CF::PPC];
-        acs_stage<CF, P>(pm, lw, flip[P], lg, drow + size_t(s) * CF::ROW);
+// v stages at phases P..v-1, the operands of stage P+1 loaded one stage ahead
+// (one basic block: the scheduler overlaps stage P+1's loads and branch
+// metrics with stage P's butterflies).
+template <class CF, int P, bool FULL>
+struct Cycle {
+    static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const uint32_t* lamrow,
+                                               const int (&flip)[CF::V], int lg, uint32_t* drow,
+                                               int s0, int nst, const XY<CF>& cur) {
+        if constexpr (P < CF::V) {
+            XY<CF> nxt = cur;
+            if constexpr (P + 1 < CF::V) {
+                if (FULL || s0 + P + 1 < nst) nxt = load_xy<CF>(lamrow, s0 + P + 1);
+            }
+            acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW);
+            if constexpr (P + 1 < CF::V) {
+                if (FULL || s0 + P + 1 < nst)
+                    Cycle<CF, P + 1, FULL>::run(pm, lamrow, flip, lg, drow, s0, nst, nxt);
+            }
+        }
     }
-}
-
-template <class CF, int... Ps>
-__device__ __forceinline__ void cycle(uint32_t (&pm)[CF::S], const uint2* lamrow,
-                                      const int (&flip)[CF::V], int lg, uint32_t* drow, int s0,
-                                      int nst, std::integer_sequence<int, Ps...>) {
-    (stage_guarded<CF, Ps>(pm, lamrow, flip, lg, drow, s0 + Ps, nst), ...);
-}
-
-// v stages without guards: one basic block, so the scheduler can overlap the
-// branch-metric chain of stage s+1 with the butterflies of stage s.
-template <class CF, int... Ps>
-__device__ __forceinline__ void cycle_full(uint32_t (&pm)[CF::S], const uint2* lamrow,
-                                           const int (&flip)[CF::V], int lg, uint32_t* drow,
-                                           std::integer_sequence<int, Ps...>) {
-    uint2 lw[sizeof...(Ps)];
-    ((lw[Ps] = lamrow[size_t(Ps) * CF::PPC]), ...);
-    (acs_stage<CF, Ps>(pm, lw[Ps], flip[Ps], lg, drow + size_t(Ps) * CF::ROW), ...);
-}
+};
 
 template <class CF, int... Ps>
 __device__ __forceinline__ void init_flips(int (&flip)[CF::V], int lg,
@@ -305,44 +328,54 @@ __device__ __forceinline__ int64_t kept_before(const FwdParams& p, int64_t s, in
 }
 
 template <class CF>
-__global__ void __launch_bounds__(CF::NT) fwd_kernel(const __grid_constant__ FwdParams p) {
+__global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(const __grid_constant__ FwdParams p) {
     constexpr int V = CF::V, N = CF::N, S = CF::S, W = CF::W, R = CF::R, T = CF::T;
-    constexpr int NT = CF::NT, BPC = CF::BPC, BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW;
-    constexpr int RAWB = CF::RAWB;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* raw = smem;
-    uint2* lam = reinterpret_cast<uint2*>(smem + CF::SMEM_RAW);
-    uint32_t* decs = reinterpret_cast<uint32_t*>(smem + CF::SMEM_RAW + CF::SMEM_LAM);
+    constexpr int BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW, RAWB = CF::RAWB, XYW = CF::XYW;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* wbase = smem + size_t(warp) * CF::WSMEM;
+    uint8_t* raw = wbase;                                                   // [BPW][RAWB]
+    uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [T][PPW][XYW]
+    uint32_t* decs = reinterpret_cast<uint32_t*>(wbase + CF::WRAW + CF::WLAM);  // [T][32][WPS]
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int lg = lane & (W - 1), grp = lane / W;
-    const bool edge = int(blockIdx.x) >= p.n_int_ctas;
-    const int e = int(blockIdx.x) - p.n_int_ctas;
+
+    // warp unit: interior warps first (BPW consecutive interior blocks), then
+    // one unit per edge block (all lane groups replicate that block)
+    const int64_t gw = int64_t(blockIdx.x) * CF::NWARP + warp;
+    const bool edge = gw >= p.n_int_warps;
+    const int e = int(gw - p.n_int_warps);
+    if (edge && e >= p.n_edge) return;
     const int span = edge ? p.edges[e].span : p.span_int;
-    const bool head = edge && (p.edges[e].flags & EDGE_HEAD);
-    const int64_t cta_b0 = int64_t(blockIdx.x) * BPC;   // launch-relative first interior block
+    const int nchunks = (span + T - 1) / T;
+    const int64_t wb0 = gw * BPW;              // launch-relative first interior block
 
     auto block_lo = [&](int i) -> int64_t {
         if (edge) return p.edges[e].lo;
-        int64_t bi = cta_b0 + i;
+        int64_t bi = wb0 + i;
         if (bi >= p.n_int) bi = p.n_int - 1;
         return (p.b_int0 + bi) * p.D - p.L;
     };
-
+    const int nblk = edge ? 1 : BPW;
     const uintptr_t vlo = reinterpret_cast<uintptr_t>(p.llr);
     const uintptr_t vhi = vlo + uintptr_t(p.n_llr);
-    // stage chunk c's raw soft values of every block of the CTA into raw[buf]
-    auto issue_raw = [&](int c, int buf) {
+
+    // 16-byte cp.async of chunk c's soft windows: lane i copies block i's
+    // window (rounded out to 16-byte vectors) to raw[c & 1][i]
+    auto issue_raw = [&](int c) {
+#ifdef PBVD_EXP_NO_INPUT
+        cp_async_commit();
+        return;
+#endif
         const int s0 = c * T;
         const int nst = min(T, span - s0);
-        for (int i = tid; i < BPC; i += NT) {
+        uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
+        for (int i = lane; i < nblk; i += 32) {
             const int64_t a = block_lo(i) + s0;
             const int64_t k0 = kept_before(p, a, R) - p.kb_ws0;
             const int64_t k1 = kept_before(p, a + nst, R) - p.kb_ws0;
-            const uintptr_t g0 = vlo + uintptr_t(k0);
-            const uintptr_t ga = g0 & ~uintptr_t(15);
+            const uintptr_t ga = (vlo + uintptr_t(k0)) & ~uintptr_t(15);
             const uintptr_t gb = (vlo + uintptr_t(k1) + 15) & ~uintptr_t(15);
-            uint8_t* dst = raw + (size_t(buf) * BPC + i) * RAWB;
+            uint8_t* dst = rb + size_t(i) * RAWB;
             for (uintptr_t x = ga; x < gb; x += 16, dst += 16) {
                 if (x >= vlo && x + 16 <= vhi) {
                     cp_async16(smem_u32(dst), reinterpret_cast<const void*>(x));
@@ -356,38 +389,109 @@ __global__ void __launch_bounds__(CF::NT) fwd_kernel(const __grid_constant__ Fwd
         }
         cp_async_commit();
     };
-    // depuncture raw[buf] into lam[stage][pair] = {A bytes r0..r3, B bytes r0..r3}
-    auto transform = [&](int c, int buf) {
+    // soft window offset (bytes) of block i in raw[.] for chunk c
+    auto win_off = [&](int i, int64_t a) -> int {
+        const int64_t kw = kept_before(p, a, R) - p.kb_ws0;
+        return int((vlo + uintptr_t(kw)) & 15);
+    };
+    // packed operands of (pair, stage) from the two signed bytes l2[h][r]
+    auto store_xy = [&](uint32_t* lb, int pr, int s, const uint32_t (&l)[R]) {
+        uint32_t wv[XYW];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t x = __vmaxs2(l[r], 0u);                   // max(lam, 0)
+            const uint32_t ny = __vadd2(~l[r], 0x00010001u);          // -lam
+            wv[2 * r] = x;
+            wv[2 * r + 1] = __vmaxs2(ny, 0u);                        // max(-lam, 0)
+        }
+#pragma unroll
+        for (int r = 2 * R; r < XYW; ++r) wv[r] = 0;
+        uint4* qq = reinterpret_cast<uint4*>(lb + (size_t(s) * PPW + pr) * XYW);
+        qq[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        if constexpr (XYW == 8) qq[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+    };
+    // Transform of chunk c, slice j of NCYC: the packed x/y operands of every
+    // (pair, stage) go to lam[c & 1][s][pair].  Unpunctured: one item = one
+    // pair x 4 stages, read as aligned words (funnel-shifted to the window
+    // offset) and split with PRMT; punctured: one item = (pair, stage).
+    auto transform = [&](int c, int j) {
         const int s0 = c * T;
         const int nst = min(T, span - s0);
-        for (int i = tid; i < BPC; i += NT) {
-            const int64_t a = block_lo(i) + s0;
-            const int64_t k0 = kept_before(p, a, R) - p.kb_ws0;
-            const int off = int((vlo + uintptr_t(k0)) & 15);
-            const uint8_t* src = raw + (size_t(buf) * BPC + i) * RAWB + off;
-            uint32_t* dst = reinterpret_cast<uint32_t*>(lam) + (i >> 1) * 2 + (i & 1);
-            if (p.P == 1) {
-                for (int s = 0; s < nst; ++s) {
-                    uint32_t v = 0;
+        const int npair = edge ? 1 : PPW;
+        const uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
+        uint32_t* lb = lam + size_t(c & 1) * T * PPW * XYW;
+        if (p.P == 1) {
+            constexpr int NQ = (T + 3) / 4;                  // quads per chunk
+            constexpr int NITEM = PPW * NQ;
+            constexpr int PER = (NITEM + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) v |= uint32_t(src[s * R + r]) << (8 * r);
-                    dst[size_t(s) * CF::PPC * 2] = v;
-                }
-            } else {
-                int ph = int(a % p.P), idx = 0;
-                for (int s = 0; s < nst; ++s) {
-                    uint32_t v = 0;
+            for (int u = 0; u < PER; ++u) {
+                const int it = (j * PER + u) * 32 + lane;
+                const int pr = it / NQ, q = it - (it / NQ) * NQ;
+                if (pr >= npair || 4 * q >= nst) continue;
+                uint32_t v[2][R];
 #pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if ((p.keep >> (r * p.P + ph)) & 1) v |= uint32_t(src[idx++]) << (8 * r);
-                    dst[size_t(s) * CF::PPC * 2] = v;
-                    ph = (ph + 1 == p.P) ? 0 : ph + 1;
+                for (int h = 0; h < 2; ++h) {
+                    const int i = edge ? 0 : 2 * pr + h;
+                    const int o = win_off(i, block_lo(i) + s0) + 4 * R * q;
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB + (o & ~3));
+                    const uint32_t sh = uint32_t(o & 3) * 8u;
+                    uint32_t wl = w[0];
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const uint32_t wh = w[k + 1];
+                        v[h][k] = __funnelshift_r(wl, wh, sh);
+                        wl = wh;
+                    }
                 }
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (4 * q + t >= nst) break;
+                    uint32_t l[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int bi = t * R + r, wdx = bi >> 2, by = bi & 3;
+                        const uint32_t sel = uint32_t(by) | (uint32_t(8 | by) << 4) |
+                                             (uint32_t(4 + by) << 8) | (uint32_t(12 + by) << 12);
+                        l[r] = prmt(v[0][wdx], v[1][wdx], sel);      // (A, B) sign-extended
+                    }
+                    store_xy(lb, pr, 4 * q + t, l);
+                }
+            }
+        } else {
+            constexpr int PER = (PPW * T + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
+#pragma unroll 1
+            for (int u = 0; u < PER; ++u) {
+                const int it = (j * PER + u) * 32 + lane;
+                const int pr = it / T, s = it - (it / T) * T;
+                if (pr >= npair || s >= nst) continue;
+                uint32_t l[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) l[r] = 0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int i = edge ? 0 : 2 * pr + h;
+                    const int64_t a = block_lo(i) + s0;
+                    const uint8_t* src = rb + size_t(i) * RAWB + win_off(i, a);
+                    const int ph0 = int(a % p.P);
+                    const int ps = ph0 + s;
+                    int idx = (ps / p.P) * p.kp + p.cum[ps % p.P] - p.cum[ph0];
+                    const int ph = ps % p.P;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const bool keep = (p.keep >> (r * p.P + ph)) & 1;
+                        const uint32_t val = keep ? uint32_t(int32_t(int8_t(src[idx++]))) : 0u;
+                        l[r] |= h ? (val << 16) : (val & 0xffffu);
+                    }
+                }
+                store_xy(lb, pr, s, l);
             }
         }
     };
 
-    // ---- per-lane constants ------------------------------------------------
+    const int lg = lane & (W - 1), grp = lane / W;
+    const bool head = edge && (p.edges[e].flags & EDGE_HEAD);
+    const int t0r = edge ? p.edges[e].t0r : p.L;     // rows below t0r are never traced
     int flip[V];
     init_flips<CF>(flip, lg, std::make_integer_sequence<int, V>{});
 
@@ -396,42 +500,53 @@ __global__ void __launch_bounds__(CF::NT) fwd_kernel(const __grid_constant__ Fwd
     for (int k = 0; k < S; ++k)
         pm[k] = head ? ((lg == 0 && k == 0) ? 0u : uint32_t(S_HEAD) * 0x00010001u) : 0u;
 
-    const uint2* lamrow = lam + warp * PPW + grp;
-    uint32_t* drow = decs + (size_t(warp) * T * 32 + lane) * CF::WPS;   // + s*ROW
+    uint32_t* drow = decs + size_t(lane) * CF::WPS;     // + s*ROW
     uint32_t* gdec = nullptr;
     if (!edge) {
-        if (cta_b0 + int64_t(warp) * BPW < p.n_int)
-            gdec = p.dec + (size_t(blockIdx.x) * CF::NWARP + warp) * size_t(p.span_int) * ROW;
-    } else if (warp == 0) {
+        gdec = p.dec + size_t(gw) * size_t(p.span_int) * ROW;
+    } else {
         gdec = p.dec_edge + size_t(e) * size_t(p.span_edge_max) * ROW;
     }
 
-    const int nchunks = (span + T - 1) / T;
-    issue_raw(0, 0);
+    issue_raw(0);
+    if (nchunks > 1) issue_raw(1);
+    if (nchunks > 1) cp_async_wait<1>(); else cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < CF::NCYC; ++j) transform(0, j);
+    __syncwarp();
     for (int c = 0; c < nchunks; ++c) {
-        if (c + 1 < nchunks) {
-            issue_raw(c + 1, (c + 1) & 1);
+        const int nst = min(T, span - c * T);
+        const bool next = c + 1 < nchunks;
+        // soft windows of chunk c+2 go in flight; those of chunk c+1 (issued a
+        // chunk ago) must have landed before this chunk's transform slices
+        if (c + 2 < nchunks) {
+            issue_raw(c + 2);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
-        transform(c, c & 1);
-        __syncthreads();
         if (c > 0) {
-            if (lane == 0) bulk_wait_read<0>();
-            __syncwarp();
+            if (lane == 0) bulk_wait_read<0>();     // survivor buffer free again
         }
-        const int nst = min(T, span - c * T);
+        __syncwarp();
+        const uint32_t* lamrow = lam + size_t(c & 1) * T * PPW * XYW + size_t(edge ? 0 : grp) * XYW;
         if (nst == T) {
 #pragma unroll 1
-            for (int s0 = 0; s0 < T; s0 += V)
-                cycle_full<CF>(pm, lamrow + size_t(s0) * CF::PPC, flip, lg,
-                               drow + size_t(s0) * ROW, std::make_integer_sequence<int, V>{});
+            for (int j = 0; j < CF::NCYC; ++j) {
+                const int s0 = j * V;
+                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, T, load_xy<CF>(lamrow, s0));
+                if (next) transform(c + 1, j);
+            }
         } else {
 #pragma unroll 1
             for (int s0 = 0; s0 < nst; s0 += V)
-                cycle<CF>(pm, lamrow, flip, lg, drow, s0, nst, std::make_integer_sequence<int, V>{});
+                Cycle<CF, 0, false>::run(pm, lamrow, flip, lg, drow, s0, nst,
+                                         load_xy<CF>(lamrow, s0));
+            if (next) {
+#pragma unroll 1
+                for (int j = 0; j < CF::NCYC; ++j) transform(c + 1, j);
+            }
         }
         // renormalise: subtract the block minimum (per 16-bit half = per block)
         uint32_t mn = pm[0];
@@ -441,12 +556,13 @@ __global__ void __launch_bounds__(CF::NT) fwd_kernel(const __grid_constant__ Fwd
         for (int o = 1; o < W; o <<= 1) mn = __vmins2(mn, __shfl_xor_sync(0xffffffffu, mn, o));
 #pragma unroll
         for (int k = 0; k < S; ++k) pm[k] -= mn;
-        // stream this chunk's survivors to HBM (one bulk copy per warp)
+        // stream this chunk's traced rows (>= t0r) to HBM: one bulk copy
+        const int r0 = max(c * T, t0r), r1 = c * T + nst;
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0 && gdec != nullptr) {
-            bulk_s2g(gdec + size_t(c) * T * ROW, smem_u32(decs + size_t(warp) * T * ROW),
-                     uint32_t(nst) * ROW * 4u);
+        if (lane == 0 && r1 > r0) {
+            bulk_s2g(gdec + size_t(r0) * ROW, smem_u32(decs + size_t(r0 - c * T) * ROW),
+                     uint32_t(r1 - r0) * ROW * 4u);
             bulk_commit();
         }
     }
@@ -468,10 +584,10 @@ __global__ void __launch_bounds__(CF::NT) fwd_kernel(const __grid_constant__ Fwd
     }
     if (lg == 0) {
         if (!edge) {
-            const int64_t bi = cta_b0 + warp * BPW + 2 * grp;
+            const int64_t bi = wb0 + 2 * grp;
             if (bi < p.n_int) p.start[bi] = int32_t(kA & 0xffu);
             if (bi + 1 < p.n_int) p.start[bi + 1] = int32_t(kB & 0xffu);
-        } else if (warp == 0 && grp == 0) {
+        } else if (grp == 0) {
             p.start_edge[e] = (p.edges[e].flags & EDGE_START0) ? 0 : int32_t(kA & 0xffu);
         }
     }

@@ -34,6 +34,7 @@ Variant make_variant(int rank) {
     v.W = W;
     for (int r = 0; r < 4; ++r) v.polys[r] = r < C::R ? C::g(r) : 0;
     v.BPC = CF::BPC;
+    v.BOXB = CF::BOXB;
     v.BPW = CF::BPW;
     v.NT = CF::NT;
     v.T = CF::T;

@@ -22,12 +22,12 @@ constexpr int EDGE_HEAD = 1;    // initial metrics: state 0 -> 0, others S_HEAD
 constexpr int EDGE_START0 = 2;  // traceback starts in state 0 (terminated tail)
 
 struct FwdParams {
-    const int8_t* llr;     // window base: first kept value of stage ws0
-    int64_t n_llr;         // valid values in the window
-    int64_t kb_ws0;        // kept values before stage ws0 (absolute index of llr[0])
+    const int8_t* llr;     // this launch's soft values (first = kept index kb_ws0)
+    int64_t n_llr;         // valid values from llr
+    int64_t kb_ws0;        // absolute kept index of llr[0]
     int64_t b_int0;        // first interior block (absolute index)
     int n_int;             // interior blocks in this launch
-    int n_int_ctas;        // CTAs for interior blocks; edge CTAs follow
+    int n_int_warps;       // warp units for interior blocks; edge units follow
     int D, L;
     int span_int;          // D + 2L
     int P;                 // puncture period (1 = none)

@@ -206,7 +206,7 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     const int64_t n_int = I1 - I0;
     const size_t edge_region_bytes = size_t(span_edge_max) * v->ROW * 4;
     const size_t edge_bytes = edge_region_bytes * MAX_EDGE + 2 * MAX_EDGE * 4 + 256;
-    const int64_t unit = std::max<int64_t>(v->BPC, 128);   // multiple of BPC and TB CTA (128)
+    const int64_t unit = std::max<int64_t>(v->BPW, 128);   // multiple of BPW and TB CTA (128)
     int64_t wave = n_int;
     if (n_int > 0) {
         const size_t budget = h->ws_limit > edge_bytes ? h->ws_limit - edge_bytes : 0;
@@ -230,9 +230,6 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         wsb + ((int_bytes + 255) & ~size_t(255)) + ((edge_bytes + 255) & ~size_t(255)));
 
     FwdParams fp{};
-    fp.llr = llr;
-    fp.n_llr = n_llr_win;
-    fp.kb_ws0 = kb_ws0;
     fp.D = int(D);
     fp.L = int(L);
     fp.span_int = span_int;
@@ -260,29 +257,89 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     tp.word_out = ((D & 31) == 0) && ((reinterpret_cast<uintptr_t>(out) & 3) == 0) &&
                   (((I0 - B0) * D) % 32 == 0);
 
-    size_t next_edge = 0;
-    int64_t done = 0;
-    bool first = true;
-    while (first || done < n_int || next_edge < edges.size()) {
-        first = false;
-        const int64_t cnt = std::min<int64_t>(wave, n_int - done);
-        const int ne = int(std::min<size_t>(MAX_EDGE, edges.size() - next_edge));
-        if (cnt <= 0 && ne == 0) break;
-        fp.b_int0 = I0 + done;
-        fp.n_int = int(std::max<int64_t>(0, cnt));
-        fp.n_int_ctas = int((std::max<int64_t>(0, cnt) + v->BPC - 1) / v->BPC);
+    // ---- launch groups: interior waves; head edges ride with the first wave,
+    // tail edges with the last, unless a group's soft window would exceed the
+    // TMA coordinate range (then edges get their own launches)
+    struct Group {
+        int64_t i0, i1;                 // interior blocks [i0, i1)
+        std::vector<EdgeDesc> edges;
+        std::vector<int64_t> eblk;      // block index of each edge
+    };
+    std::vector<Group> groups;
+    for (int64_t d0 = 0; d0 < n_int || (n_int == 0 && groups.empty()); d0 += wave) {
+        groups.push_back({I0 + d0, I0 + std::min(n_int, d0 + wave), {}, {}});
+        if (n_int == 0) break;
+    }
+    const int64_t n_head = I0 - B0;
+    for (size_t k = 0; k < edges.size(); ++k) {
+        Group& g = (int64_t(k) < n_head) ? groups.front() : groups.back();
+        g.edges.push_back(edges[k]);
+        g.eblk.push_back(int64_t(k) < n_head ? B0 + int64_t(k) : I1 + (int64_t(k) - n_head));
+    }
+    auto group_range = [&](const Group& g, int64_t& klo, int64_t& khi) {
+        int64_t slo = INT64_MAX, shi = -1;
+        if (g.i1 > g.i0) {
+            slo = geo(h, n_info, n_stages, nb, g.i0).lo;
+            shi = geo(h, n_info, n_stages, nb, g.i1 - 1).hi;
+        }
+        for (const auto& ed : g.edges) {
+            slo = std::min(slo, ed.lo);
+            shi = std::max(shi, ed.lo + ed.span);
+        }
+        klo = kept_before_h(h, slo);
+        khi = kept_before_h(h, shi);
+    };
+    const int64_t kLimit = (int64_t(1) << 31) - 4096;
+    {   // split oversized groups / too many edges
+        std::vector<Group> out;
+        for (auto& g : groups) {
+            int64_t klo, khi;
+            group_range(g, klo, khi);
+            const bool big = (khi - klo) > kLimit;
+            Group core{g.i0, g.i1, {}, {}};
+            std::vector<Group> extra;
+            for (size_t k = 0; k < g.edges.size(); ++k) {
+                Group* tgt = nullptr;
+                if (!big && core.edges.size() < size_t(MAX_EDGE)) tgt = &core;
+                if (!tgt) {
+                    if (extra.empty() || extra.back().edges.size() >= size_t(MAX_EDGE))
+                        extra.push_back({0, 0, {}, {}});
+                    tgt = &extra.back();
+                }
+                tgt->edges.push_back(g.edges[k]);
+                tgt->eblk.push_back(g.eblk[k]);
+            }
+            if (core.i1 > core.i0 || !core.edges.empty()) out.push_back(core);
+            for (auto& x : extra) out.push_back(x);
+        }
+        groups.swap(out);
+    }
+
+    for (const Group& g : groups) {
+        const int64_t cnt = g.i1 - g.i0;
+        const int ne = int(g.edges.size());
+        int64_t klo, khi;
+        group_range(g, klo, khi);
+        if (khi - klo > kLimit + 4096)
+            return fail(h, PBVD_EUNSUPPORTED, "a single block's soft window exceeds 2 GiB");
+        fp.llr = llr + (klo - kb_ws0);
+        fp.kb_ws0 = klo;
+        fp.n_llr = khi - klo;
+        fp.b_int0 = g.i0;
+        fp.n_int = int(cnt);
+        fp.n_int_warps = int((cnt + v->BPW - 1) / v->BPW);
         fp.n_edge = ne;
         tp.n_int = fp.n_int;
-        tp.n_int_ctas = int((std::max<int64_t>(0, cnt) + 127) / 128);
-        tp.out_bit0 = (I0 + done - B0) * D;
+        tp.n_int_ctas = int((cnt + 127) / 128);
+        tp.out_bit0 = (g.i0 - B0) * D;
         tp.n_edge = ne;
         for (int i = 0; i < ne; ++i) {
-            fp.edges[i] = edges[next_edge + i];
-            tp.edges[i] = edges[next_edge + i];
+            fp.edges[i] = g.edges[size_t(i)];
+            tp.edges[i] = g.edges[size_t(i)];
         }
         const int ev = record(h, stream);
         if (ev >= 0) cudaEventRecord(h->ev_pool[ev], stream);
-        v->fwd(fp.n_int_ctas + ne, stream, fp);
+        v->fwd(int((fp.n_int_warps + ne + v->NT / 32 - 1) / (v->NT / 32)), stream, fp);
         if (ev >= 0) {
             cudaEventRecord(h->ev_pool[ev + 1], stream);
             h->ev_fwd.push_back({ev, ev + 1});
@@ -297,8 +354,6 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         h->launches += 2;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
-        done += std::max<int64_t>(0, cnt);
-        next_edge += size_t(ne);
     }
     return PBVD_OK;
 }

@@ -16,7 +16,7 @@ namespace pbvd {
 struct Variant {
     int K, R, W;
     uint32_t polys[4];
-    int BPC, BPW, NT, T, ROW, NR_TB, TT;
+    int BPC, BPW, NT, T, ROW, NR_TB, TT, BOXB;
     size_t smem_fwd, smem_tb;
     int default_rank;   // lower = preferred default for the code
     cudaError_t (*prepare)();
