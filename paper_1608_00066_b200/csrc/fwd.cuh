@@ -95,9 +95,10 @@ struct Cfg {
     static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
     static constexpr int SLICE = (PPW + NCYC - 1) / NCYC;  // pairs transformed per cycle
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
+    static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
     static constexpr size_t WLAM = size_t(2) * T * PPW * XYW * 4;  // double buffered
     static constexpr size_t WDEC = size_t(T) * ROW * 4;
-    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEC + 127) / 128) * 128;
+    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEC + WDEP + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
 
     // alpha of the butterfly whose E slot has register index k, restricted
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     uint8_t* raw = wbase;                                                   // [BPW][RAWB]
     uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [T][PPW][XYW]
     uint32_t* decs = reinterpret_cast<uint32_t*>(wbase + CF::WRAW + CF::WLAM);  // [T][32][WPS]
+    uint8_t* dep = wbase + CF::WRAW + CF::WLAM + CF::WDEC;                  // [BPW][RAWB]
 
 
     // warp unit: interior warps first (BPW consecutive interior blocks), then
@@ -394,6 +396,34 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         const int64_t kw = kept_before(p, a, R) - p.kb_ws0;
         return int((vlo + uintptr_t(kw)) & 15);
     };
+    // punctured codes: expand chunk c's kept values of every block to a dense
+    // [stage][r] byte window in dep[block] (erasure = 0), lane = block (c-18)
+    auto depuncture = [&](int c) {
+        const int s0 = c * T;
+        const int nst = min(T, span - s0);
+        const uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
+        for (int i = lane; i < nblk; i += 32) {
+            const int64_t a = block_lo(i) + s0;
+            const uint8_t* src = rb + size_t(i) * RAWB + win_off(i, a);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(i) * RAWB);
+            int ph = int(a % p.P), idx = 0, nb = 0;
+            uint32_t acc = 0;
+            for (int st = 0; st < nst; ++st) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const bool keep = (p.keep >> (r * p.P + ph)) & 1;
+                    const uint32_t val = keep ? uint32_t(src[idx++]) : 0u;
+                    acc |= val << (8 * (nb & 3));
+                    if ((++nb & 3) == 0) {
+                        dst[(nb >> 2) - 1] = acc;
+                        acc = 0;
+                    }
+                }
+                ph = (ph + 1 == p.P) ? 0 : ph + 1;
+            }
+            if (nb & 3) dst[nb >> 2] = acc;
+        }
+    };
     // packed operands of (pair, stage) from the two signed bytes l2[h][r]
     auto store_xy = [&](uint32_t* lb, int pr, int s, const uint32_t (&l)[R]) {
         uint32_t wv[XYW];
@@ -418,73 +448,44 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         const int s0 = c * T;
         const int nst = min(T, span - s0);
         const int npair = edge ? 1 : PPW;
-        const uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
+        const bool dense = (p.P == 1);            // else read the depunctured dep[]
+        const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
         uint32_t* lb = lam + size_t(c & 1) * T * PPW * XYW;
-        if (p.P == 1) {
-            constexpr int NQ = (T + 3) / 4;                  // quads per chunk
-            constexpr int NITEM = PPW * NQ;
-            constexpr int PER = (NITEM + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
+        constexpr int NQ = (T + 3) / 4;                  // quads per chunk
+        constexpr int NITEM = PPW * NQ;
+        constexpr int PER = (NITEM + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
 #pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int it = (j * PER + u) * 32 + lane;
-                const int pr = it / NQ, q = it - (it / NQ) * NQ;
-                if (pr >= npair || 4 * q >= nst) continue;
-                uint32_t v[2][R];
+        for (int u = 0; u < PER; ++u) {
+            const int it = (j * PER + u) * 32 + lane;
+            const int pr = it / NQ, q = it - (it / NQ) * NQ;
+            if (pr >= npair || 4 * q >= nst) continue;
+            uint32_t v[2][R];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int i = edge ? 0 : 2 * pr + h;
-                    const int o = win_off(i, block_lo(i) + s0) + 4 * R * q;
-                    const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB + (o & ~3));
-                    const uint32_t sh = uint32_t(o & 3) * 8u;
-                    uint32_t wl = w[0];
+            for (int h = 0; h < 2; ++h) {
+                const int i = edge ? 0 : 2 * pr + h;
+                const int o = (dense ? win_off(i, block_lo(i) + s0) : 0) + 4 * R * q;
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB + (o & ~3));
+                const uint32_t sh = uint32_t(o & 3) * 8u;
+                uint32_t wl = w[0];
 #pragma unroll
-                    for (int k = 0; k < R; ++k) {
-                        const uint32_t wh = w[k + 1];
-                        v[h][k] = __funnelshift_r(wl, wh, sh);
-                        wl = wh;
-                    }
-                }
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    if (4 * q + t >= nst) break;
-                    uint32_t l[R];
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int bi = t * R + r, wdx = bi >> 2, by = bi & 3;
-                        const uint32_t sel = uint32_t(by) | (uint32_t(8 | by) << 4) |
-                                             (uint32_t(4 + by) << 8) | (uint32_t(12 + by) << 12);
-                        l[r] = prmt(v[0][wdx], v[1][wdx], sel);      // (A, B) sign-extended
-                    }
-                    store_xy(lb, pr, 4 * q + t, l);
+                for (int k = 0; k < R; ++k) {
+                    const uint32_t wh = w[k + 1];
+                    v[h][k] = __funnelshift_r(wl, wh, sh);
+                    wl = wh;
                 }
             }
-        } else {
-            constexpr int PER = (PPW * T + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
-#pragma unroll 1
-            for (int u = 0; u < PER; ++u) {
-                const int it = (j * PER + u) * 32 + lane;
-                const int pr = it / T, s = it - (it / T) * T;
-                if (pr >= npair || s >= nst) continue;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (4 * q + t >= nst) break;
                 uint32_t l[R];
 #pragma unroll
-                for (int r = 0; r < R; ++r) l[r] = 0;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int i = edge ? 0 : 2 * pr + h;
-                    const int64_t a = block_lo(i) + s0;
-                    const uint8_t* src = rb + size_t(i) * RAWB + win_off(i, a);
-                    const int ph0 = int(a % p.P);
-                    const int ps = ph0 + s;
-                    int idx = (ps / p.P) * p.kp + p.cum[ps % p.P] - p.cum[ph0];
-                    const int ph = ps % p.P;
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const bool keep = (p.keep >> (r * p.P + ph)) & 1;
-                        const uint32_t val = keep ? uint32_t(int32_t(int8_t(src[idx++]))) : 0u;
-                        l[r] |= h ? (val << 16) : (val & 0xffffu);
-                    }
+                for (int r = 0; r < R; ++r) {
+                    const int bi = t * R + r, wdx = bi >> 2, by = bi & 3;
+                    const uint32_t sel = uint32_t(by) | (uint32_t(8 | by) << 4) |
+                                         (uint32_t(4 + by) << 8) | (uint32_t(12 + by) << 12);
+                    l[r] = prmt(v[0][wdx], v[1][wdx], sel);      // (A, B) sign-extended
                 }
-                store_xy(lb, pr, s, l);
+                store_xy(lb, pr, 4 * q + t, l);
             }
         }
     };
@@ -512,6 +513,10 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     if (nchunks > 1) issue_raw(1);
     if (nchunks > 1) cp_async_wait<1>(); else cp_async_wait<0>();
     __syncwarp();
+    if (p.P != 1) {
+        depuncture(0);
+        __syncwarp();
+    }
 #pragma unroll 1
     for (int j = 0; j < CF::NCYC; ++j) transform(0, j);
     __syncwarp();
@@ -530,6 +535,10 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             if (lane == 0) bulk_wait_read<0>();     // survivor buffer free again
         }
         __syncwarp();
+        if (next && p.P != 1) {
+            depuncture(c + 1);
+            __syncwarp();
+        }
         const uint32_t* lamrow = lam + size_t(c & 1) * T * PPW * XYW + size_t(edge ? 0 : grp) * XYW;
         if (nst == T) {
 #pragma unroll 1
