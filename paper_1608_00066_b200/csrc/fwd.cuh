@@ -195,6 +195,27 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
     if constexpr (S >= 16) {
 #pragma unroll
         for (int kw = 0; kw < WPS; ++kw) {
+#if PBVD_PACK_TREE
+            // P_m: bytes = sign of [t(m).A, t(8+m).A, t(m).B, t(8+m).B] (0x00/0xFF)
+            uint32_t P[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) P[m] = prmt(t[16 * kw + m], t[16 * kw + 8 + m], SEL);
+            // bit m of every byte from P_m: a 3-level LOP3 tree (depth 3, 7 ops)
+            uint32_t w2[4], w4[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t M = 0x01010101u << (2 * i);       // bit 2i from P[2i]
+                w2[i] = (P[2 * i] & M) | (P[2 * i + 1] & ~M);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const uint32_t M = 0x03030303u << (4 * i);       // bits 4i,4i+1 from w2[2i]
+                w4[i] = (w2[2 * i] & M) | (w2[2 * i + 1] & ~M);
+            }
+            words[kw] = ((w4[0] & 0x0F0F0F0Fu) | (w4[1] & 0xF0F0F0F0u)) ^ inv;
+#else
+            // P_m: bytes = sign of [t(m).A, t(8+m).A, t(m).B, t(8+m).B] (0x00/0xFF);
+            // bit m of every byte from P_m by a chain of LOP3 merges
             uint32_t wd = prmt(t[16 * kw], t[16 * kw + 8], SEL);
 #pragma unroll
             for (int m = 1; m < 8; ++m) {
@@ -203,6 +224,7 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
                 wd = (wd & M) | (pm & ~M);
             }
             words[kw] = wd ^ inv;
+#endif
         }
     } else {
         constexpr int H = S / 2;
@@ -228,9 +250,24 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
 }
 
 // One trellis stage at compile-time phase P (Eq. 1 per output state).
+// Pipe balancing: the decision operand t = E + BM_own + C - m_other is an
+// IADD3 (ALU pipe) for outputs with FMA_OUT(k) false, and two IMADs (FMA
+// pipe: E + (BM_own + C), then - m_other) otherwise, so the ALU pipe --
+// which also carries VIADDMNMX, PRMT and LOP3 -- is not the only one busy.
+#ifndef PBVD_PACK_TREE
+#define PBVD_PACK_TREE 0
+#endif
+#ifndef PBVD_FMA_SPLIT
+#define PBVD_FMA_SPLIT 1
+#endif
+template <class CF>
+__host__ __device__ constexpr bool fma_out(int k) {
+    return PBVD_FMA_SPLIT == 0 ? false : PBVD_FMA_SPLIT == 1 ? (k & 1) != 0 : (k % 3) != 0;
+}
+
 template <class CF, int P>
 __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
-                                          int lg, uint32_t* drow) {
+                                          int lg, uint32_t* drow, uint32_t one, uint32_t neg1) {
     using C = typename CF::code;
     constexpr int S = CF::S, NC = CF::NC;
     constexpr int g0 = C::g0, gK = C::gK;
@@ -254,7 +291,9 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             // x = 1: min(E + BM(beta), O + BM(theta))         (Eqs. 4, 6)
             const uint32_t mO1 = add32(O, Pv[a ^ gK ^ g0]);
             const uint32_t nO = __viaddmin_s16x2(E, Pv[a ^ gK], mO1);
-            const uint32_t tO = sub_add(E, mO1, PC[a ^ gK]);
+            uint32_t tO;
+            if constexpr (fma_out<CF>(1)) tO = imad(mO1, neg1, imad(E, one, PC[a ^ gK]));
+            else tO = sub_add(E, mO1, PC[a ^ gK]);
             pm[k] = nE;
             pm[k | pb] = nO;
             t[k] = tE;
@@ -289,7 +328,8 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             const uint32_t own = pm[k];
             const uint32_t mR = add32(recv[k], Pr[a]);
             pm[k] = __viaddmin_s16x2(own, Po[a], mR);
-            t[k] = sub_add(own, mR, PCo[a]);
+            if (fma_out<CF>(k)) t[k] = imad(mR, neg1, imad(own, one, PCo[a]));
+            else t[k] = sub_add(own, mR, PCo[a]);
         }
         pack_store<CF>(t, 0u - lb, drow);
     }
@@ -302,16 +342,17 @@ template <class CF, int P, bool FULL>
 struct Cycle {
     static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const uint32_t* lamrow,
                                                const int (&flip)[CF::V], int lg, uint32_t* drow,
-                                               int s0, int nst, const XY<CF>& cur) {
+                                               int s0, int nst, const XY<CF>& cur, uint32_t one,
+                                               uint32_t neg1) {
         if constexpr (P < CF::V) {
             XY<CF> nxt = cur;
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst) nxt = load_xy<CF>(lamrow, s0 + P + 1);
             }
-            acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW);
+            acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW, one, neg1);
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst)
-                    Cycle<CF, P + 1, FULL>::run(pm, lamrow, flip, lg, drow, s0, nst, nxt);
+                    Cycle<CF, P + 1, FULL>::run(pm, lamrow, flip, lg, drow, s0, nst, nxt, one, neg1);
             }
         }
     }
@@ -544,14 +585,15 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
 #pragma unroll 1
             for (int j = 0; j < CF::NCYC; ++j) {
                 const int s0 = j * V;
-                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, T, load_xy<CF>(lamrow, s0));
+                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, T, load_xy<CF>(lamrow, s0),
+                                        p.one, p.neg_one);
                 if (next) transform(c + 1, j);
             }
         } else {
 #pragma unroll 1
             for (int s0 = 0; s0 < nst; s0 += V)
                 Cycle<CF, 0, false>::run(pm, lamrow, flip, lg, drow, s0, nst,
-                                         load_xy<CF>(lamrow, s0));
+                                         load_xy<CF>(lamrow, s0), p.one, p.neg_one);
             if (next) {
 #pragma unroll 1
                 for (int j = 0; j < CF::NCYC; ++j) transform(c + 1, j);

@@ -30,6 +30,7 @@ struct FwdParams {
     int n_int_warps;       // warp units for interior blocks; edge units follow
     int D, L;
     int span_int;          // D + 2L
+    uint32_t one, neg_one; // 1 and 0xffffffff, opaque to the compiler (pipe balancing)
     int P;                 // puncture period (1 = none)
     int kp;                // kept values per period
     uint64_t keep;         // keep flag of (r, p) at bit r*P + p

@@ -233,6 +233,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     fp.D = int(D);
     fp.L = int(L);
     fp.span_int = span_int;
+    fp.one = 1u;
+    fp.neg_one = 0xffffffffu;
     fp.P = h->P;
     fp.kp = h->kp;
     fp.keep = h->keep;

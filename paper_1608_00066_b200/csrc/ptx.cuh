@@ -24,6 +24,13 @@ __device__ __forceinline__ uint32_t sub_add(uint32_t a, uint32_t b, uint32_t c) 
         : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
 }
+// a * m + c on the FMA pipe (IMAD): with m an opaque +-1 this is an add or a
+// subtract that ptxas cannot move to the ALU pipe
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t m, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(m), "r"(c));
+    return d;
+}
 // a + b (plain 32-bit add; exact 16x2 add for non-negative halves)
 __device__ __forceinline__ uint32_t add32(uint32_t a, uint32_t b) {
     uint32_t d;
