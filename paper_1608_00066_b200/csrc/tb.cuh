@@ -15,11 +15,16 @@
 //
 // The walk tracks the PHYSICAL slot q of the current state (the forward
 // kernel stores logical state u of stage s+1 at q = rotl_v(u, (s+1) mod v)):
-// with p = s mod v, the decoded bit (state >> (v-1), Alg. 1) is
-// bit p of q, and the predecessor 2*(state mod 2^{v-1}) + sp (line 225) is
-// q with bit p replaced by the survivor bit sp -- no rotation per step.
-// Both candidate survivor words of the predecessor are loaded one step ahead,
-// so the dependent chain per step is a select and a shift, not a smem load.
+// with p = s mod v, the predecessor 2*(state mod 2^{v-1}) + sp (Alg. 1 line
+// 225) is q with bit p replaced by the survivor bit sp -- no rotation.  The
+// decoded bit of stage s (state >> (v-1), line 222) is bit p of q, which is
+// exactly the survivor bit read at stage s+v: the output is the survivor-bit
+// sequence delayed by v stages, so the walk shifts every survivor bit into a
+// 32-bit accumulator and stores it as the output word once 32 bits are
+// complete (the walk stops v stages above the decoding block's start).
+// Chunks are aligned to multiples of v so full chunks run with compile-time
+// phases; both candidate survivor words of the predecessor are loaded one step
+// ahead, so the dependent chain per step is a select and a shift.
 #pragma once
 #include <cstdint>
 #include "params.h"
@@ -34,23 +39,87 @@ struct TbCfg {
     static constexpr int ROW = CF::ROW;                     // words per stage per region
     static constexpr int NBUF = 4;                          // ring depth (chunks)
     static constexpr int TT0 = 65536 / (NBUF * NR * ROW * 4);
-    static constexpr int TT = TT0 >= 32 ? 32 : (TT0 >= 16 ? 16 : 8);
+    static constexpr int TTR = TT0 >= 32 ? 32 : (TT0 >= 16 ? 16 : 8);
+    static constexpr int TT = (TTR / CF::V) * CF::V;        // chunk rows, a multiple of v
+    static_assert(TT >= CF::V, "traceback chunk");
     static constexpr size_t RING = size_t(NBUF) * NR * TT * ROW * 4;
     static constexpr size_t SMEM = RING + 64;
+    // bit of q above which the word index starts (q >> WSH selects the word)
+    static constexpr int WSH = CF::S >= 16 ? 4 : ilog2(CF::S);
 };
 
 template <class CF>
 __device__ __forceinline__ uint32_t tb_word_index(uint32_t q, int woff) {
-    if constexpr (CF::S >= 16) return uint32_t(woff) + (q >> 4);
-    else return uint32_t(woff) + (q >> ilog2(CF::S));
+    return uint32_t(woff) + (q >> TbCfg<CF>::WSH);
 }
 template <class CF>
-__device__ __forceinline__ uint32_t tb_bitpos(uint32_t q, uint32_t h) {
-    if constexpr (CF::S >= 16) return 16u * h + (q & 15u);
+__device__ __forceinline__ uint32_t tb_bitpos(uint32_t q, uint32_t hbit) {
+    if constexpr (CF::S >= 16) return hbit + (q & 15u);
     else {
         constexpr int LH = ilog2(CF::S / 2);
-        return 16u * h + 8u * ((q >> LH) & 1u) + (q & uint32_t(CF::S / 2 - 1));
+        return hbit + 8u * ((q >> LH) & 1u) + (q & uint32_t(CF::S / 2 - 1));
     }
+}
+
+struct TbState {
+    uint32_t q;        // physical slot of the current state
+    uint32_t wcur;     // survivor word holding q's bit in the current row
+    uint32_t acc;      // last 32 survivor bits, newest in bit 0
+    int cnt;           // steps until the next output word is complete
+    int e;             // s - t0r - v of the current row
+};
+
+// One step at row s with compile-time phase PH: the survivor bit of q, the
+// output accumulator, the predecessor slot and its survivor word (from the two
+// candidates of row s-1 at nrow).
+template <class CF, int PH>
+__device__ __forceinline__ void tb_step(TbState& t, const uint32_t* nrow, int woff, uint32_t hbit,
+                                        uint32_t* out32, int64_t word0, int nwords) {
+    constexpr uint32_t pb = 1u << PH;
+    uint32_t w0, w1;
+    if constexpr (PH >= TbCfg<CF>::WSH) {
+        w0 = nrow[tb_word_index<CF>(t.q & ~pb, woff)];
+        w1 = nrow[tb_word_index<CF>(t.q | pb, woff)];
+    } else {
+        w0 = w1 = nrow[tb_word_index<CF>(t.q, woff)];
+    }
+    const uint32_t dec = (t.wcur >> tb_bitpos<CF>(t.q, hbit)) & 1u;
+    t.acc = (t.acc << 1) | dec;
+    if (t.cnt == 0 && t.e >= 0 && (t.e >> 5) < nwords) out32[word0 + (t.e >> 5)] = t.acc;
+    t.cnt = (t.cnt - 1) & 31;
+    --t.e;
+    t.q = (t.q & ~pb) | (dec << PH);
+    if constexpr (PH >= TbCfg<CF>::WSH) t.wcur = dec ? w1 : w0;
+    else t.wcur = w0;
+}
+
+// the same with a runtime phase (partial chunks)
+template <class CF>
+__device__ __forceinline__ void tb_step_rt(TbState& t, int ph, const uint32_t* nrow, int woff,
+                                           uint32_t hbit, uint32_t* out32, int64_t word0,
+                                           int nwords) {
+    const uint32_t pb = 1u << ph;
+    const uint32_t w0 = nrow[tb_word_index<CF>(t.q & ~pb, woff)];
+    const uint32_t w1 = nrow[tb_word_index<CF>(t.q | pb, woff)];
+    const uint32_t dec = (t.wcur >> tb_bitpos<CF>(t.q, hbit)) & 1u;
+    t.acc = (t.acc << 1) | dec;
+    if (t.cnt == 0 && t.e >= 0 && (t.e >> 5) < nwords) out32[word0 + (t.e >> 5)] = t.acc;
+    t.cnt = (t.cnt - 1) & 31;
+    --t.e;
+    t.q = (t.q & ~pb) | (dec << ph);
+    t.wcur = dec ? w1 : w0;
+}
+
+// v steps, phases v-1 .. 0, from row `row` (phase v-1) downwards; the last
+// step's predecessor row is `last_below`
+template <class CF, int PH>
+__device__ __forceinline__ void tb_cycle(TbState& t, const uint32_t*& row,
+                                         const uint32_t* last_below, int woff, uint32_t hbit,
+                                         uint32_t* out32, int64_t word0, int nwords) {
+    const uint32_t* nrow = (PH == 0) ? last_below : row - CF::ROW;
+    tb_step<CF, PH>(t, nrow, woff, hbit, out32, word0, nwords);
+    row = nrow;
+    if constexpr (PH > 0) tb_cycle<CF, PH - 1>(t, row, last_below, woff, hbit, out32, word0, nwords);
 }
 
 template <class CF>
@@ -110,86 +179,127 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
     }
     __syncthreads();
 
-    const int nrows = span - t0r;
-    const int nchunks = (nrows + TT - 1) / TT;
-    // chunk j holds rows [max(t0r, span-(j+1)TT), span-j*TT) at buffer offset
-    // row - (span - (j+1)TT)
-    auto issue = [&](int j) {
-        const int rhi = span - j * TT;
-        const int rlo = max(t0r, rhi - TT);
-        const uint32_t bytes = uint32_t(rhi - rlo) * ROW * 4u;
-        const int buf = j % NBUF;
+    // rows walked: [s_min, span); chunk c holds rows [c*TT, c*TT+TT) (clipped)
+    const int s_min = min(span, t0r + V);
+    const int c_top = (span - 1) / TT;
+    const int c_bot = s_min / TT;
+    const int nchunks = (s_min < span) ? c_top - c_bot + 1 : 0;
+    auto chunk_rows = [&](int k, int& lo, int& hi) {        // k-th chunk walked
+        const int c = c_top - k;
+        lo = max(c * TT, s_min);
+        hi = min(c * TT + TT, span);
+    };
+    auto slot_row = [&](int k, int r) -> const uint32_t* {  // row r of chunk k
+        const int c = c_top - k;
+        return ring + ((size_t(k % NBUF) * NR + rloc) * TT + (r - c * TT)) * ROW;
+    };
+    auto issue = [&](int k) {
+        int lo, hi;
+        chunk_rows(k, lo, hi);
+        const uint32_t bytes = uint32_t(hi - lo) * ROW * 4u;
         if (tid < nreg) {
-            const uint32_t mb = smem_u32(&mbar[buf]);
+            const uint32_t mb = smem_u32(&mbar[k % NBUF]);
+            const int c = c_top - k;
             mbar_arrive_expect_tx(mb, bytes);
-            bulk_g2s(smem_u32(ring + ((size_t(buf) * NR + tid) * TT + (rlo - (rhi - TT))) * ROW),
-                     rbase + size_t(tid) * rstride + size_t(rlo) * ROW, bytes, mb);
+            bulk_g2s(smem_u32(ring + ((size_t(k % NBUF) * NR + tid) * TT + (lo - c * TT)) * ROW),
+                     rbase + size_t(tid) * rstride + size_t(lo) * ROW, bytes, mb);
         }
     };
-    auto wait = [&](int j) {
-        mbar_wait(smem_u32(&mbar[j % NBUF]), uint32_t(j / NBUF) & 1u);
-    };
-    // row pointer of stage s (for this thread's region and pair group)
-    const int woff = g * W * WPS;
-    auto rowp = [&](int s) -> const uint32_t* {
-        const int j = (span - 1 - s) / TT;
-        const int off = s - (span - (j + 1) * TT);
-        return ring + ((size_t(j % NBUF) * NR + rloc) * TT + off) * ROW;
-    };
+    auto wait = [&](int k) { mbar_wait(smem_u32(&mbar[k % NBUF]), uint32_t(k / NBUF) & 1u); };
 
-    for (int j = 0; j < min(NBUF - 1, nchunks); ++j) issue(j);
+    for (int k = 0; k < min(NBUF - 1, nchunks); ++k) issue(k);
 
-    // physical slot of the start state at stage `span` (phase span mod v)
+    // start state's physical slot at stage `span` (phase span mod v)
     const int pe = span % V;
-    uint32_t q = ((uint32_t(st) << pe) | (uint32_t(st) >> (V - pe))) & uint32_t(CF::N - 1);
-    int ph = (span - 1) % V;                     // phase of row s = span-1
-    uint32_t acc = 0;
-    uint32_t* out32 = reinterpret_cast<uint32_t*>(p.out);
+    TbState t;
+    t.q = ((uint32_t(st) << pe) | (uint32_t(st) >> (V - pe))) & uint32_t(CF::N - 1);
+    // decoded bits of the top v stages come from the start state itself:
+    // acc bit i = "survivor bit of stage span+i" := bit ((span+i) mod v) of q
+    t.acc = 0;
+    for (int i = V - 1; i >= 0; --i) t.acc = (t.acc << 1) | ((t.q >> ((span + i) % V)) & 1u);
+    t.e = (span - 1) - t0r - V;
+    t.cnt = ((t.e % 32) + 32) % 32;
+    t.wcur = 0;
+    const uint32_t hbit = 16u * uint32_t(h);
+    const int woff = g * W * WPS;
+    const int nbits = t1r - t0r;
+    // words: interior blocks store aligned 32-bit words; edge blocks stage
+    // their (possibly partial) words through a local buffer and store bytes
     const bool words = (!edge) && p.word_out;
-    uint32_t wcur = 0;
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(p.out);
+    const int64_t word0 = out_bit0 >> 5;
+    const int nwords = (nbits + 31) >> 5;
 
-    // one step of Alg. 1 K2 at row s (phase ph): decoded bit, predecessor
-    // slot, and the predecessor's survivor word from the preloaded candidates
-    auto step = [&](const uint32_t* nrow, int s) {
-        const uint32_t pb = 1u << ph;
-        const uint32_t w0 = nrow[tb_word_index<CF>(q & ~pb, woff)];
-        const uint32_t w1 = nrow[tb_word_index<CF>(q | pb, woff)];
-        const uint32_t dec = (wcur >> tb_bitpos<CF>(q, uint32_t(h))) & 1u;
-        acc = (acc << 1) | ((q >> ph) & 1u);
-        const int eb = s - t0r;                      // emitted bit index (s < t1r)
-        if (s < t1r) {
-            if (words) {
-                if ((eb & 31) == 0) out32[(out_bit0 + eb) >> 5] = acc;
-            } else if ((eb & 7) == 0) {
-                p.out[(out_bit0 + eb) >> 3] = uint8_t(acc & 0xffu);
+    if (!words) {
+        // edge blocks / unaligned output: plain per-step walk with byte stores
+        // (every thread of the CTA takes part in the ring and its barriers)
+        int ph = (span - 1) % V;
+        uint32_t q = t.q;
+        uint32_t bacc = 0;
+        for (int k = 0; k < nchunks; ++k) {
+            if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
+            wait(k);
+            int lo, hi;
+            chunk_rows(k, lo, hi);
+            if (active) {
+                for (int s = hi - 1; s >= lo; --s) {
+                    const uint32_t* row = slot_row(k, s);
+                    const uint32_t wd = row[tb_word_index<CF>(q, woff)];
+                    const uint32_t dec = (wd >> tb_bitpos<CF>(q, hbit)) & 1u;
+                    if (s < t1r) {
+                        bacc = (bacc << 1) | ((q >> ph) & 1u);
+                        const int eb = s - t0r;
+                        if ((eb & 7) == 0) p.out[(out_bit0 + eb) >> 3] = uint8_t(bacc & 0xffu);
+                    }
+                    q = (q & ~(1u << ph)) | (dec << ph);
+                    ph = (ph == 0) ? V - 1 : ph - 1;
+                }
             }
+            __syncthreads();
         }
-        q = (q & ~pb) | (dec << ph);
-        wcur = dec ? w1 : w0;
-        ph = (ph == 0) ? V - 1 : ph - 1;
-    };
-
-    for (int j = 0; j < nchunks; ++j) {
-        // chunk j and j+1 resident (the walk looks one row ahead)
-        if (j + NBUF - 1 < nchunks) issue(j + NBUF - 1);
-        wait(j);
-        if (j + 1 < nchunks) wait(j + 1);
-        const int rhi = span - j * TT;
-        const int rlo = max(t0r, rhi - TT);
+        // rows below s_min: their (< v) decoded bits are still held in q
         if (active) {
-            const uint32_t* row = rowp(rhi - 1);
-            if (j == 0) wcur = row[tb_word_index<CF>(q, woff)];
-            // the row below the chunk: next chunk's top row (any valid smem
-            // address at the very bottom -- its words are never used)
-            const uint32_t* below = (j + 1 < nchunks) ? rowp(rlo - 1) : row;
-#pragma unroll 4
-            for (int s = rhi - 1; s > rlo; --s) {
-                row -= ROW;
-                step(row, s);
+            for (int s = s_min - 1; s >= t0r; --s) {
+                if (s < t1r) {
+                    bacc = (bacc << 1) | ((q >> ph) & 1u);
+                    const int eb = s - t0r;
+                    if ((eb & 7) == 0) p.out[(out_bit0 + eb) >> 3] = uint8_t(bacc & 0xffu);
+                }
+                ph = (ph == 0) ? V - 1 : ph - 1;
             }
-            step(below, rlo);
         }
-        __syncthreads();          // slot j % NBUF free for chunk j + NBUF
+        return;
+    }
+
+    for (int k = 0; k < nchunks; ++k) {
+        // chunk k and k+1 resident (the walk looks one row ahead)
+        if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
+        wait(k);
+        if (k + 1 < nchunks) wait(k + 1);
+        int lo, hi;
+        chunk_rows(k, lo, hi);
+        if (active) {
+            const uint32_t* row = slot_row(k, hi - 1);
+            if (k == 0) t.wcur = row[tb_word_index<CF>(t.q, woff)];
+            const uint32_t* below = (k + 1 < nchunks) ? slot_row(k + 1, lo - 1) : row;
+            const int c = c_top - k;
+            if (hi - lo == TT && lo == c * TT) {
+                // full, v-aligned chunk: TT/v cycles with compile-time phases
+#pragma unroll 1
+                for (int cy = 0; cy < TT / V - 1; ++cy)
+                    tb_cycle<CF, V - 1>(t, row, row - V * ROW, woff, hbit, out32, word0, nwords);
+                tb_cycle<CF, V - 1>(t, row, below, woff, hbit, out32, word0, nwords);
+            } else {
+                int ph = (hi - 1) % V;
+                for (int s = hi - 1; s >= lo; --s) {
+                    const uint32_t* nrow = (s > lo) ? row - ROW : below;
+                    tb_step_rt<CF>(t, ph, nrow, woff, hbit, out32, word0, nwords);
+                    row = nrow;
+                    ph = (ph == 0) ? V - 1 : ph - 1;
+                }
+            }
+        }
+        __syncthreads();          // slot k % NBUF free for chunk k + NBUF
     }
 }
 
