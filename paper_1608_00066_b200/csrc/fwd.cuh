@@ -98,7 +98,8 @@ struct Cfg {
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
     static constexpr size_t WLAM = size_t(2) * T * PPW * XYW * 4;  // double buffered
     static constexpr size_t WDEC = size_t(T) * ROW * 4;
-    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEC + WDEP + 127) / 128) * 128;
+    static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
+    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEC + WDEP + WOFF + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
 
     // alpha of the butterfly whose E slot has register index k, restricted
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [T][PPW][XYW]
     uint32_t* decs = reinterpret_cast<uint32_t*>(wbase + CF::WRAW + CF::WLAM);  // [T][32][WPS]
     uint8_t* dep = wbase + CF::WRAW + CF::WLAM + CF::WDEC;                  // [BPW][RAWB]
+    uint8_t* woffs = dep + CF::WDEP;                                        // [2][BPW]
 
 
     // warp unit: interior warps first (BPW consecutive interior blocks), then
@@ -415,17 +417,25 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         for (int i = lane; i < nblk; i += 32) {
             const int64_t a = block_lo(i) + s0;
             const int64_t k0 = kept_before(p, a, R) - p.kb_ws0;
-            const int64_t k1 = kept_before(p, a + nst, R) - p.kb_ws0;
             const uintptr_t ga = (vlo + uintptr_t(k0)) & ~uintptr_t(15);
-            const uintptr_t gb = (vlo + uintptr_t(k1) + 15) & ~uintptr_t(15);
             uint8_t* dst = rb + size_t(i) * RAWB;
-            for (uintptr_t x = ga; x < gb; x += 16, dst += 16) {
-                if (x >= vlo && x + 16 <= vhi) {
-                    cp_async16(smem_u32(dst), reinterpret_cast<const void*>(x));
-                } else {
-                    for (int j = 0; j < 16; ++j) {
-                        const uintptr_t y = x + j;
-                        dst[j] = (y >= vlo && y < vhi) ? *reinterpret_cast<const uint8_t*>(y) : 0;
+            woffs[(c & 1) * BPW + i] = uint8_t((vlo + uintptr_t(k0)) & 15);
+            if (ga >= vlo && ga + RAWB <= vhi) {
+                // interior fast path: a fixed number of 16-byte vectors
+#pragma unroll
+                for (int j = 0; j < RAWB / 16; ++j)
+                    cp_async16(smem_u32(dst + 16 * j), reinterpret_cast<const void*>(ga + 16 * j));
+            } else {
+                const int64_t k1 = kept_before(p, a + max(nst, 0), R) - p.kb_ws0;
+                const uintptr_t gb = (vlo + uintptr_t(k1) + 15) & ~uintptr_t(15);
+                for (uintptr_t x = ga; x < gb; x += 16, dst += 16) {
+                    if (x >= vlo && x + 16 <= vhi) {
+                        cp_async16(smem_u32(dst), reinterpret_cast<const void*>(x));
+                    } else {
+                        for (int j = 0; j < 16; ++j) {
+                            const uintptr_t y = x + j;
+                            dst[j] = (y >= vlo && y < vhi) ? *reinterpret_cast<const uint8_t*>(y) : 0;
+                        }
                     }
                 }
             }
@@ -487,24 +497,28 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     // offset) and split with PRMT; punctured: one item = (pair, stage).
     auto transform = [&](int c, int j) {
         const int s0 = c * T;
-        const int nst = min(T, span - s0);
+        const int nst = min(T, span - s0);           // <= 0 past the last chunk: no stores
         const int npair = edge ? 1 : PPW;
         const bool dense = (p.P == 1);            // else read the depunctured dep[]
         const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
+        const uint8_t* wo = woffs + (c & 1) * BPW;
         uint32_t* lb = lam + size_t(c & 1) * T * PPW * XYW;
         constexpr int NQ = (T + 3) / 4;                  // quads per chunk
         constexpr int NITEM = PPW * NQ;
         constexpr int PER = (NITEM + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
+        // straight-line (predicated stores, no branches) so that it schedules
+        // together with the ACS cycle it follows
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
             const int it = (j * PER + u) * 32 + lane;
-            const int pr = it / NQ, q = it - (it / NQ) * NQ;
-            if (pr >= npair || 4 * q >= nst) continue;
+            const int pr0 = it / NQ, q = it - (it / NQ) * NQ;
+            const bool valid = pr0 < npair;
+            const int pr = valid ? pr0 : 0;
             uint32_t v[2][R];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int i = edge ? 0 : 2 * pr + h;
-                const int o = (dense ? win_off(i, block_lo(i) + s0) : 0) + 4 * R * q;
+                const int o = (dense ? int(wo[i]) : 0) + 4 * R * q;
                 const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB + (o & ~3));
                 const uint32_t sh = uint32_t(o & 3) * 8u;
                 uint32_t wl = w[0];
@@ -517,7 +531,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                if (4 * q + t >= nst) break;
                 uint32_t l[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -526,7 +539,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                                          (uint32_t(4 + by) << 8) | (uint32_t(12 + by) << 12);
                     l[r] = prmt(v[0][wdx], v[1][wdx], sel);      // (A, B) sign-extended
                 }
-                store_xy(lb, pr, 4 * q + t, l);
+                if (valid && 4 * q + t < nst) store_xy(lb, pr, 4 * q + t, l);
             }
         }
     };
@@ -587,7 +600,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                 const int s0 = j * V;
                 Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, T, load_xy<CF>(lamrow, s0),
                                         p.one, p.neg_one);
-                if (next) transform(c + 1, j);
+                transform(c + 1, j);     // harmless past the last chunk
             }
         } else {
 #pragma unroll 1
