@@ -255,6 +255,9 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
 // IADD3 (ALU pipe) for outputs with FMA_OUT(k) false, and two IMADs (FMA
 // pipe: E + (BM_own + C), then - m_other) otherwise, so the ALU pipe --
 // which also carries VIADDMNMX, PRMT and LOP3 -- is not the only one busy.
+#ifndef PBVD_L2_HINTS
+#define PBVD_L2_HINTS 0
+#endif
 #ifndef PBVD_PACK_TREE
 #define PBVD_PACK_TREE 0
 #endif
@@ -603,8 +606,13 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                 transform(c + 1, j);     // harmless past the last chunk
             }
         } else {
+            // partial (last) chunk: whole cycles unguarded, then the remainder
+            int s0 = 0;
 #pragma unroll 1
-            for (int s0 = 0; s0 < nst; s0 += V)
+            for (; s0 + V <= nst; s0 += V)
+                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, nst, load_xy<CF>(lamrow, s0),
+                                        p.one, p.neg_one);
+            if (s0 < nst)
                 Cycle<CF, 0, false>::run(pm, lamrow, flip, lg, drow, s0, nst,
                                          load_xy<CF>(lamrow, s0), p.one, p.neg_one);
             if (next) {
@@ -625,8 +633,13 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0 && r1 > r0) {
+#if PBVD_L2_HINTS
+            bulk_s2g_hint(gdec + size_t(r0) * ROW, smem_u32(decs + size_t(r0 - c * T) * ROW),
+                          uint32_t(r1 - r0) * ROW * 4u, policy_evict_last());
+#else
             bulk_s2g(gdec + size_t(r0) * ROW, smem_u32(decs + size_t(r0 - c * T) * ROW),
                      uint32_t(r1 - r0) * ROW * 4u);
+#endif
             bulk_commit();
         }
     }

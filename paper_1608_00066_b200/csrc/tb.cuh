@@ -201,8 +201,14 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
             const uint32_t mb = smem_u32(&mbar[k % NBUF]);
             const int c = c_top - k;
             mbar_arrive_expect_tx(mb, bytes);
+#if PBVD_L2_HINTS
+            bulk_g2s_hint(smem_u32(ring + ((size_t(k % NBUF) * NR + tid) * TT + (lo - c * TT)) * ROW),
+                          rbase + size_t(tid) * rstride + size_t(lo) * ROW, bytes, mb,
+                          policy_evict_first());
+#else
             bulk_g2s(smem_u32(ring + ((size_t(k % NBUF) * NR + tid) * TT + (lo - c * TT)) * ROW),
                      rbase + size_t(tid) * rstride + size_t(lo) * ROW, bytes, mb);
+#endif
         }
     };
     auto wait = [&](int k) { mbar_wait(smem_u32(&mbar[k % NBUF]), uint32_t(k / NBUF) & 1u); };
