@@ -37,8 +37,8 @@ struct TbCfg {
     static constexpr int NT = 128;                          // blocks per CTA
     static constexpr int NR = NT / CF::BPW;                 // regions per CTA
     static constexpr int ROW = CF::ROW;                     // words per stage per region
-    static constexpr int NBUF = 4;                          // ring depth (chunks)
-    static constexpr int TT0 = 65536 / (NBUF * NR * ROW * 4);
+    static constexpr int NBUF = 3;                          // ring depth (chunks)
+    static constexpr int TT0 = 98304 / (NBUF * NR * ROW * 4);
     static constexpr int TTR = TT0 >= 32 ? 32 : (TT0 >= 16 ? 16 : 8);
     static constexpr int TT = (TTR / CF::V) * CF::V;        // chunk rows, a multiple of v
     static_assert(TT >= CF::V, "traceback chunk");
@@ -64,7 +64,8 @@ __device__ __forceinline__ uint32_t tb_bitpos(uint32_t q, uint32_t hbit) {
 struct TbState {
     uint32_t q;        // physical slot of the current state
     uint32_t wcur;     // survivor word holding q's bit in the current row
-    uint32_t acc;      // last 32 survivor bits, newest in bit 0
+    uint32_t acc;      // last 32 survivor bits, newest in bit 0 (per-step path)
+    uint64_t acc64;    // last 64 survivor bits (cycle path)
     int cnt;           // steps until the next output word is complete
     int e;             // s - t0r - v of the current row
 };
@@ -73,8 +74,7 @@ struct TbState {
 // output accumulator, the predecessor slot and its survivor word (from the two
 // candidates of row s-1 at nrow).
 template <class CF, int PH>
-__device__ __forceinline__ void tb_step(TbState& t, const uint32_t* nrow, int woff, uint32_t hbit,
-                                        uint32_t* out32, int64_t word0, int nwords) {
+__device__ __forceinline__ void tb_step(TbState& t, const uint32_t* nrow, int woff, uint32_t hbit) {
     constexpr uint32_t pb = 1u << PH;
     uint32_t w0, w1;
     if constexpr (PH >= TbCfg<CF>::WSH) {
@@ -84,10 +84,7 @@ __device__ __forceinline__ void tb_step(TbState& t, const uint32_t* nrow, int wo
         w0 = w1 = nrow[tb_word_index<CF>(t.q, woff)];
     }
     const uint32_t dec = (t.wcur >> tb_bitpos<CF>(t.q, hbit)) & 1u;
-    t.acc = (t.acc << 1) | dec;
-    if (t.cnt == 0 && t.e >= 0 && (t.e >> 5) < nwords) out32[word0 + (t.e >> 5)] = t.acc;
-    t.cnt = (t.cnt - 1) & 31;
-    --t.e;
+    t.acc64 = (t.acc64 << 1) | dec;
     t.q = (t.q & ~pb) | (dec << PH);
     if constexpr (PH >= TbCfg<CF>::WSH) t.wcur = dec ? w1 : w0;
     else t.wcur = w0;
@@ -102,9 +99,9 @@ __device__ __forceinline__ void tb_step_rt(TbState& t, int ph, const uint32_t* n
     const uint32_t w0 = nrow[tb_word_index<CF>(t.q & ~pb, woff)];
     const uint32_t w1 = nrow[tb_word_index<CF>(t.q | pb, woff)];
     const uint32_t dec = (t.wcur >> tb_bitpos<CF>(t.q, hbit)) & 1u;
-    t.acc = (t.acc << 1) | dec;
-    if (t.cnt == 0 && t.e >= 0 && (t.e >> 5) < nwords) out32[word0 + (t.e >> 5)] = t.acc;
-    t.cnt = (t.cnt - 1) & 31;
+    t.acc64 = (t.acc64 << 1) | dec;
+    if ((t.e & 31) == 0 && t.e >= 0 && (t.e >> 5) < nwords)
+        out32[word0 + (t.e >> 5)] = uint32_t(t.acc64);
     --t.e;
     t.q = (t.q & ~pb) | (dec << ph);
     t.wcur = dec ? w1 : w0;
@@ -113,13 +110,25 @@ __device__ __forceinline__ void tb_step_rt(TbState& t, int ph, const uint32_t* n
 // v steps, phases v-1 .. 0, from row `row` (phase v-1) downwards; the last
 // step's predecessor row is `last_below`
 template <class CF, int PH>
+__device__ __forceinline__ void tb_steps(TbState& t, const uint32_t*& row,
+                                         const uint32_t* last_below, int woff, uint32_t hbit) {
+    const uint32_t* nrow = (PH == 0) ? last_below : row - CF::ROW;
+    tb_step<CF, PH>(t, nrow, woff, hbit);
+    row = nrow;
+    if constexpr (PH > 0) tb_steps<CF, PH - 1>(t, row, last_below, woff, hbit);
+}
+// one cycle plus the output: at most one 32-bit word completes per cycle
+// (v <= 8 < 32); it is the accumulator shifted back to the completing step
+template <class CF>
 __device__ __forceinline__ void tb_cycle(TbState& t, const uint32_t*& row,
                                          const uint32_t* last_below, int woff, uint32_t hbit,
                                          uint32_t* out32, int64_t word0, int nwords) {
-    const uint32_t* nrow = (PH == 0) ? last_below : row - CF::ROW;
-    tb_step<CF, PH>(t, nrow, woff, hbit, out32, word0, nwords);
-    row = nrow;
-    if constexpr (PH > 0) tb_cycle<CF, PH - 1>(t, row, last_below, woff, hbit, out32, word0, nwords);
+    tb_steps<CF, CF::V - 1>(t, row, last_below, woff, hbit);
+    const int eb = t.e, ea = t.e - CF::V;          // steps had e = eb .. ea+1
+    const int w = eb >> 5;                         // floor (eb >= 0 checked below)
+    if (eb >= 0 && (w << 5) > ea && w < nwords)
+        out32[word0 + w] = uint32_t(t.acc64 >> ((w << 5) - ea - 1));
+    t.e = ea;
 }
 
 template <class CF>
@@ -221,10 +230,11 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
     t.q = ((uint32_t(st) << pe) | (uint32_t(st) >> (V - pe))) & uint32_t(CF::N - 1);
     // decoded bits of the top v stages come from the start state itself:
     // acc bit i = "survivor bit of stage span+i" := bit ((span+i) mod v) of q
+    t.acc64 = 0;
+    for (int i = V - 1; i >= 0; --i) t.acc64 = (t.acc64 << 1) | ((t.q >> ((span + i) % V)) & 1u);
     t.acc = 0;
-    for (int i = V - 1; i >= 0; --i) t.acc = (t.acc << 1) | ((t.q >> ((span + i) % V)) & 1u);
     t.e = (span - 1) - t0r - V;
-    t.cnt = ((t.e % 32) + 32) % 32;
+    t.cnt = 0;
     t.wcur = 0;
     const uint32_t hbit = 16u * uint32_t(h);
     const int woff = g * W * WPS;
@@ -293,8 +303,8 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
                 // full, v-aligned chunk: TT/v cycles with compile-time phases
 #pragma unroll 1
                 for (int cy = 0; cy < TT / V - 1; ++cy)
-                    tb_cycle<CF, V - 1>(t, row, row - V * ROW, woff, hbit, out32, word0, nwords);
-                tb_cycle<CF, V - 1>(t, row, below, woff, hbit, out32, word0, nwords);
+                    tb_cycle<CF>(t, row, row - V * ROW, woff, hbit, out32, word0, nwords);
+                tb_cycle<CF>(t, row, below, woff, hbit, out32, word0, nwords);
             } else {
                 int ph = (hi - 1) % V;
                 for (int s = hi - 1; s >= lo; --s) {
