@@ -118,3 +118,23 @@ def test_config_full_size_bit_exact(pbvd, orc, cfg):
     # and the decoder actually decodes: BER in the expected range
     ber = (unpack(got, c["n_info"]) != info.cpu().numpy()).mean()
     assert ber < (2e-2 if c["hard"] else 1e-4)
+
+
+def test_compute_sanitizer_memcheck_clean(pbvd):
+    """memcheck over a small decode of each kernel family (edge blocks, lane
+    stages, punctured input) reports no error and stays bit-exact."""
+    import shutil
+    import subprocess
+    import sys
+    from pathlib import Path
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not Path(cs).exists():
+        pytest.skip("compute-sanitizer not available")
+    root = Path(__file__).resolve().parents[1]
+    for args in (["k7", "3000", "64", "20", "2"], ["k7", "2000", "96", "30", "4", "3/4"],
+                 ["k9", "1500", "64", "20", "8"]):
+        r = subprocess.run([cs, "--tool", "memcheck", "--error-exitcode", "9", sys.executable,
+                            str(root / "tools" / "debug_case.py"), *args],
+                           capture_output=True, text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        assert "bad bytes: 0" in r.stdout
