@@ -669,6 +669,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         }
     }
     if (lane == 0) bulk_wait<0>();
+    pdl_launch_dependents();   // the traceback grid may start scheduling
 }
 
 }  // namespace pbvd

@@ -18,9 +18,23 @@ template <class CF>
 void launch_fwd(int grid, cudaStream_t s, const FwdParams& p) {
     fwd_kernel<CF><<<grid, CF::NT, CF::SMEM, s>>>(p);
 }
+// The traceback is launched with programmatic stream serialization (PDL):
+// its CTAs may be scheduled as soon as every forward CTA has signalled
+// griddepcontrol.launch_dependents, and it waits (griddepcontrol.wait) for
+// the forward grid's memory before touching survivors.
 template <class CF>
 void launch_tb(int grid, cudaStream_t s, const TbParams& p) {
-    tb_kernel<CF><<<grid, TbCfg<CF>::NT, TbCfg<CF>::SMEM, s>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(TbCfg<CF>::NT);
+    cfg.dynamicSmemBytes = TbCfg<CF>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tb_kernel<CF>, p);
 }
 
 template <class C, int W>

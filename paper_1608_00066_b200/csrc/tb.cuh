@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
         g = (tid % BPW) >> 1;
         h = tid & 1;
         out_bit0 = p.out_bit0 + i * p.D;
-        st = active ? p.start[i] : 0;
+        st = 0;
     } else {
         span = p.edges[e].span;
         t0r = p.edges[e].t0r;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
         g = 0;
         h = 0;
         out_bit0 = p.edges[e].out_bit0;
-        st = p.start_edge[e];
+        st = 0;
     }
 
     if (tid == 0) {
@@ -187,6 +187,13 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();          // the forward grid's survivors and start states are complete
+    if (!edge) {
+        const int64_t i = int64_t(blockIdx.x) * TC::NT + tid;
+        if (active) st = p.start[i];
+    } else {
+        st = p.start_edge[e];
+    }
 
     // rows walked: [s_min, span); chunk c holds rows [c*TT, c*TT+TT) (clipped)
     const int s_min = min(span, t0r + V);

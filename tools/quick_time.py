@@ -24,4 +24,12 @@ for lanes in sorted({l for (K, R, p, l) in P.supported() if K == code["K"] and t
     ts.sort(); fw.sort(); tb.sort()
     ms = ts[len(ts)//2]
     ber = (torch.unpackbits if hasattr(torch,'unpackbits') else None)
-    print(f"{cfg} n_info={n_info} lanes={lanes}: {ms:.3f} ms  {n_info/ms/1e6:.2f} Gb/s  fwd {fw[5]:.3f} ms tb {tb[5]:.3f} ms  launches={n}", flush=True)
+    dec.set_profiling(False)
+    ts2 = []
+    for i in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); dec.decode(llr, n_info, out=out); e1.record(); torch.cuda.synchronize()
+        ts2.append(e0.elapsed_time(e1))
+    ts2.sort()
+    ms2 = ts2[len(ts2)//2]
+    print(f"{cfg} n_info={n_info} lanes={lanes}: {ms:.3f} ms  {n_info/ms/1e6:.2f} Gb/s  fwd {fw[5]:.3f} ms tb {tb[5]:.3f} ms  launches={n}  | no-prof {ms2:.3f} ms {n_info/ms2/1e6:.2f} Gb/s", flush=True)
