@@ -1,5 +1,5 @@
 // fwd.cuh -- forward kernel of the PBVD on sm_100a: branch metrics + ACS +
-// decision packing + bulk store of survivors + final argmin per block.
+// decision packing + survivor store + final argmin per block.
 //
 // Paper mapping (PAPER.md line numbers "P:n"):
 //   ACS recursion, Eq. 1; encoder / trellis, Eq. 2 and the shift
@@ -21,24 +21,27 @@
 //     rotate once per stage, so no data moves for register bits; when bit p
 //     is a lane bit the partner values are fetched with one SHFL.BFLY per
 //     register.
-//   * path metrics use a non-negative branch metric BM+(c) = BM(c) +
-//     sum_r max(-lam_r, 0) (a per-stage constant shift of the canonical
-//     metric, reading c-4: every decision and tie is identical) and are
-//     re-normalised by the block minimum every T stages, so all values stay
-//     in [0, 32767] (reading c-20) and plain 32-bit adds are exact 16x2 adds.
+//   * path metrics use the non-negative biased branch metric
+//     BM'(c) = BM(c) + 128R = sum_r (c_r ? lam_r + 128 : 128) in [0, 255R]
+//     (a constant shift of the canonical metric, reading c-4: every decision
+//     and tie is identical) and are re-normalised by the block minimum every
+//     T stages, so all values stay in [0, 32767] (reading c-20) and plain
+//     32-bit adds are exact 16x2 adds.
 //   * ACS per output: 1 add (other candidate), 1 VIADDMNMX.S16x2 (the fused
-//     add+min -- Blackwell DPX), 1 IADD3 producing m_own - m_other + 0x7FFF
-//     whose per-half sign bit is the decision (m_other < m_own, tie -> upper).
+//     add+min -- Blackwell DPX), 1 IADD3 (or 2 IMADs, FMA pipe) producing
+//     m_own - m_other + 0x7FFF whose per-half sign bit is the decision
+//     (m_other < m_own, tie -> upper).
 //   * decisions: sign bits of 2 registers -> 4 bytes via PRMT sign-replicate,
-//     8 such words merged by LOP3 into one 32-bit word (32 decisions), stored
-//     to shared memory; each warp streams T stages of survivors to HBM with
-//     one cp.async.bulk (TMA engine) per chunk.
+//     8 such words merged by LOP3 into one 32-bit word (32 decisions); each
+//     lane stores its WPS words of a stage straight to HBM (a warp writes
+//     32*WPS contiguous words per stage, full 128-byte lines).
 //   * every warp is an autonomous pipeline (no CTA barrier anywhere): it
 //     copies its blocks' soft windows of the NEXT chunk with 16-byte cp.async
-//     (LDGSTS) while it computes the current one, then depunctures them into
-//     per-stage, per-pair packed 16x2 operands x_r = max(lam_r,0),
-//     y_r = max(-lam_r,0) in shared memory, read with one 16/32-byte LDS per
-//     stage one stage ahead of use.
+//     (LDGSTS) while it computes the current one, then (depunctured if
+//     needed) interleaves them into per-(pair, stage) words of biased bytes
+//     u_r = lam_r + 128 for both blocks, read with one LDS per stage one stage
+//     ahead of use and zero-extended to 16x2 by PRMT.  Shared memory per warp
+//     is ~12 KB, so occupancy is set by registers, not shared memory.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -84,22 +87,33 @@ struct Cfg {
     static constexpr int BPC = NWARP * BPW;   // blocks per CTA
     static constexpr int PPC = NWARP * PPW;   // pairs per CTA
     static constexpr int T = V * (32 / V);    // stages per chunk = normalisation period
+    // int16 headroom of the biased metric BM'(c) = BM(c) + 128R in [0, 255R]
+    // (reading c-4): PMs start a chunk at <= M0 = max(S_HEAD, v*128R) and grow
+    // by <= 255R per stage, so after k <= T stages every PM, every E + BM and
+    // every decision operand E + BM_own - m_other lies within +-(M0 + T*255R),
+    // which must fit int16 (reading c-20)
+    static_assert(cmax(S_HEAD, V * 128 * R) + T * 255 * R <= 32767, "int16 headroom");
     // raw window per block and chunk: the T*R soft bytes rounded out to
-    // 16-byte vectors; an odd number of 16-byte vectors per window keeps both
-    // the cp.async writes and the transform's byte reads bank-conflict free
+    // 16-byte vectors (+1 vector for the alignment superset)
     static constexpr int BOXB = ((T * R + 15) / 16) * 16 + 16;
     static constexpr int RAWB = ((BOXB / 16) & 1) ? BOXB : BOXB + 16;
     static constexpr int ROW = 32 * WPS;      // survivor words per stage per region
-    static constexpr int XYW = (R == 2) ? 4 : 8;   // packed x/y words per pair-stage
-    // per warp: raw windows [BPW][RAWB], operands [T][PPW][XYW], survivors [T][32][WPS]
+    // per (pair, stage): LW words of biased soft bytes [uA_2k, uB_2k, uA_2k+1, uB_2k+1]
+    static constexpr int LW = (R + 1) / 2;
+    // transform item = (pair, G stages): G*R bytes = whole words per block
+    static constexpr int G = (R % 4 == 0) ? 1 : (R % 2 == 0) ? 2 : 4;
+    static constexpr int NG = (T + G - 1) / G;                  // groups per chunk
+    // operand row of a pair: T*LW words, padded by 32/PPW words so that the
+    // PPW rows start in distinct banks (conflict-free per-stage reads across
+    // pairs) and, for PPW <= 16, stay 8-byte aligned for the transform stores
+    static constexpr int LSTR = ((NG * G * LW + 31) / 32) * 32 + 32 / PPW;
+    // per warp: raw windows [2][BPW][RAWB], operands [2][PPW][LSTR], depunctured [BPW][RAWB]
     static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
-    static constexpr int SLICE = (PPW + NCYC - 1) / NCYC;  // pairs transformed per cycle
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
-    static constexpr size_t WLAM = size_t(2) * T * PPW * XYW * 4;  // double buffered
-    static constexpr size_t WDEC = size_t(T) * ROW * 4;
+    static constexpr size_t WLAM = size_t(2) * PPW * LSTR * 4;     // double buffered
     static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
-    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEC + WDEP + WOFF + 127) / 128) * 128;
+    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
 
     // alpha of the butterfly whose E slot has register index k, restricted
@@ -134,51 +148,54 @@ __device__ __forceinline__ int lane_alpha(int lg) {
     return a;
 }
 
-// x/y operands of one stage for a block pair: xy[2r] = x_r, xy[2r+1] = y_r
+// biased soft bytes of one stage for a block pair (LW words, see Cfg::LW)
 template <class CF>
 struct XY {
-    uint32_t v[CF::XYW];
+    uint32_t v[CF::LW];
 };
 
 template <class CF>
 __device__ __forceinline__ XY<CF> load_xy(const uint32_t* lamrow, int s) {
     XY<CF> r;
-    const uint4* q = reinterpret_cast<const uint4*>(lamrow + size_t(s) * CF::PPW * CF::XYW);
-    const uint4 a = q[0];
-    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
-    if constexpr (CF::XYW == 8) {
-        const uint4 b = q[1];
-        r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+    if constexpr (CF::LW == 1) {
+        r.v[0] = lamrow[s];
+    } else {
+        const uint2 a = *reinterpret_cast<const uint2*>(lamrow + 2 * s);
+        r.v[0] = a.x; r.v[1] = a.y;
     }
     return r;
 }
 
-// The 2^R non-negative codeword metrics of one stage for a block pair,
-// permuted by the lane's alpha offset: Pv[c] = BM+(c ^ flip), where
-//   BM+(c) = sum_r (c_r ? max(lam_r,0) : max(-lam_r,0))   (c-4, canonical + const)
+// The 2^R codeword metrics of one stage for a block pair, permuted by the
+// lane's alpha offset: Pv[c] = BM'(c ^ flip) with the biased metric
+//   BM'(c) = sum_r (c_r ? u_r : 128),  u_r = lam_r + 128 in [0, 255]
+// = BM(c) + 128 R (a constant shift of the canonical metric, reading c-4).
+// u_r is zero-extended to 16x2 straight from the stored bytes by PRMT; a lane
+// whose alpha offset flips bit r takes (128, u_r) instead of (u_r, 128) by a
+// per-lane PRMT selector (hoisted out of the loop by the compiler).
 template <class CF, int POSS>
 __device__ __forceinline__ void bm_vector(const XY<CF>& xy, int flip, uint32_t (&Pv)[CF::NC]) {
     constexpr int R = CF::R;
+    constexpr uint32_t K128 = 0x00800080u;
+    const uint32_t kb = 0x80u;                    // PRMT byte 4 = 0x80, byte 5 = 0
     uint32_t x[R], y[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        x[r] = xy.v[2 * r];
-        y[r] = xy.v[2 * r + 1];
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
+        const uint32_t su = (r & 1) ? 0x5352u : 0x5150u;   // [u_A, 0, u_B, 0]
         if ((POSS >> r) & 1) {
-            const uint32_t fm = 0u - uint32_t((flip >> r) & 1);
-            const uint32_t nx = (x[r] & ~fm) | (y[r] & fm);
-            y[r] = (y[r] & ~fm) | (x[r] & fm);
-            x[r] = nx;
+            const bool f = (flip >> r) & 1;
+            x[r] = prmt(xy.v[r >> 1], kb, f ? 0x5454u : su);
+            y[r] = prmt(xy.v[r >> 1], kb, f ? su : 0x5454u);
+        } else {
+            x[r] = prmt(xy.v[r >> 1], kb, su);
+            y[r] = K128;
         }
     }
 #pragma unroll
     for (int c = 0; c < CF::NC; ++c) {
         uint32_t s = ((c & 1) ? x[0] : y[0]);
 #pragma unroll
-        for (int r = 1; r < R; ++r) s = add32(s, ((c >> r) & 1) ? x[r] : y[r]);
+        for (int r = 1; r < R; ++r) s += ((c >> r) & 1) ? x[r] : y[r];
         Pv[c] = s;
     }
 }
@@ -376,16 +393,15 @@ __device__ __forceinline__ int64_t kept_before(const FwdParams& p, int64_t s, in
 template <class CF>
 __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(const __grid_constant__ FwdParams p) {
     constexpr int V = CF::V, N = CF::N, S = CF::S, W = CF::W, R = CF::R, T = CF::T;
-    constexpr int BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW, RAWB = CF::RAWB, XYW = CF::XYW;
+    constexpr int BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW, RAWB = CF::RAWB;
+    constexpr int LW = CF::LW, G = CF::G, NG = CF::NG, LSTR = CF::LSTR;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* wbase = smem + size_t(warp) * CF::WSMEM;
-    uint8_t* raw = wbase;                                                   // [BPW][RAWB]
-    uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [T][PPW][XYW]
-    uint32_t* decs = reinterpret_cast<uint32_t*>(wbase + CF::WRAW + CF::WLAM);  // [T][32][WPS]
-    uint8_t* dep = wbase + CF::WRAW + CF::WLAM + CF::WDEC;                  // [BPW][RAWB]
+    uint8_t* raw = wbase;                                                   // [2][BPW][RAWB]
+    uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [2][PPW][LSTR]
+    uint8_t* dep = wbase + CF::WRAW + CF::WLAM;                             // [BPW][RAWB]
     uint8_t* woffs = dep + CF::WDEP;                                        // [2][BPW]
-
 
     // warp unit: interior warps first (BPW consecutive interior blocks), then
     // one unit per edge block (all lane groups replicate that block)
@@ -478,78 +494,79 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             if (nb & 3) dst[nb >> 2] = acc;
         }
     };
-    // packed operands of (pair, stage) from the two signed bytes l2[h][r]
-    auto store_xy = [&](uint32_t* lb, int pr, int s, const uint32_t (&l)[R]) {
-        uint32_t wv[XYW];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const uint32_t x = __vmaxs2(l[r], 0u);                   // max(lam, 0)
-            const uint32_t ny = __vadd2(~l[r], 0x00010001u);          // -lam
-            wv[2 * r] = x;
-            wv[2 * r + 1] = __vmaxs2(ny, 0u);                        // max(-lam, 0)
-        }
-#pragma unroll
-        for (int r = 2 * R; r < XYW; ++r) wv[r] = 0;
-        uint4* qq = reinterpret_cast<uint4*>(lb + (size_t(s) * PPW + pr) * XYW);
-        qq[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        if constexpr (XYW == 8) qq[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-    };
-    // Transform of chunk c, slice j of NCYC: the packed x/y operands of every
-    // (pair, stage) go to lam[c & 1][s][pair].  Unpunctured: one item = one
-    // pair x 4 stages, read as aligned words (funnel-shifted to the window
-    // offset) and split with PRMT; punctured: one item = (pair, stage).
+    // Transform of chunk c, slice j of NCYC: the soft bytes of every (pair,
+    // stage) are interleaved A/B, biased by +128 (u = lam ^ 0x80) and stored
+    // as LW words to lam[c & 1][pair][stage].  One item = (pair, G stages) =
+    // G*R/4 whole words per block, read as aligned words funnel-shifted to the
+    // window offset; consecutive lanes take consecutive groups of one pair
+    // (conflict-free reads and 8/16-byte stores).
     auto transform = [&](int c, int j) {
-        const int s0 = c * T;
-        const int nst = min(T, span - s0);           // <= 0 past the last chunk: no stores
         const int npair = edge ? 1 : PPW;
         const bool dense = (p.P == 1);            // else read the depunctured dep[]
         const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
         const uint8_t* wo = woffs + (c & 1) * BPW;
-        uint32_t* lb = lam + size_t(c & 1) * T * PPW * XYW;
-        constexpr int NQ = (T + 3) / 4;                  // quads per chunk
-        constexpr int NITEM = PPW * NQ;
+        uint32_t* lb = lam + size_t(c & 1) * PPW * LSTR;
+        constexpr int GW = G * R / 4;                     // words per block per item
+        constexpr int NITEM = PPW * NG;
         constexpr int PER = (NITEM + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
-        // straight-line (predicated stores, no branches) so that it schedules
-        // together with the ACS cycle it follows
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
             const int it = (j * PER + u) * 32 + lane;
-            const int pr0 = it / NQ, q = it - (it / NQ) * NQ;
+            const int pr0 = it / NG, g = it - (it / NG) * NG;
             const bool valid = pr0 < npair;
             const int pr = valid ? pr0 : 0;
-            uint32_t v[2][R];
+            uint32_t v[2][GW];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int i = edge ? 0 : 2 * pr + h;
-                const int o = (dense ? int(wo[i]) : 0) + 4 * R * q;
+                const int o = (dense ? int(wo[i]) : 0) + 4 * GW * g;
                 const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB + (o & ~3));
                 const uint32_t sh = uint32_t(o & 3) * 8u;
                 uint32_t wl = w[0];
 #pragma unroll
-                for (int k = 0; k < R; ++k) {
+                for (int k = 0; k < GW; ++k) {
                     const uint32_t wh = w[k + 1];
-                    v[h][k] = __funnelshift_r(wl, wh, sh);
+                    v[h][k] = __funnelshift_r(wl, wh, sh) ^ 0x80808080u;   // u = lam + 128
                     wl = wh;
                 }
             }
+            uint32_t ow[G * LW];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                uint32_t l[R];
+            for (int t = 0; t < G; ++t) {
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int bi = t * R + r, wdx = bi >> 2, by = bi & 3;
-                    const uint32_t sel = uint32_t(by) | (uint32_t(8 | by) << 4) |
-                                         (uint32_t(4 + by) << 8) | (uint32_t(12 + by) << 12);
-                    l[r] = prmt(v[0][wdx], v[1][wdx], sel);      // (A, B) sign-extended
+                for (int q = 0; q < LW; ++q) {
+                    const int ia = t * R + 2 * q;
+                    const int ib = (2 * q + 1 < R) ? ia + 1 : ia;      // pad byte
+                    if ((ia >> 2) == (ib >> 2)) {
+                        const uint32_t sel = uint32_t(ia & 3) | (uint32_t(4 + (ia & 3)) << 4) |
+                                             (uint32_t(ib & 3) << 8) | (uint32_t(4 + (ib & 3)) << 12);
+                        ow[t * LW + q] = prmt(v[0][ia >> 2], v[1][ia >> 2], sel);
+                    } else {
+                        const uint32_t s2 = uint32_t(ia & 3) | (uint32_t(4 + (ib & 3)) << 4);
+                        const uint32_t xa = prmt(v[0][ia >> 2], v[0][ib >> 2], s2);
+                        const uint32_t xb = prmt(v[1][ia >> 2], v[1][ib >> 2], s2);
+                        ow[t * LW + q] = prmt(xa, xb, 0x5140u);
+                    }
                 }
-                if (valid && 4 * q + t < nst) store_xy(lb, pr, 4 * q + t, l);
+            }
+            if (valid) {
+                uint32_t* dst = lb + size_t(pr) * LSTR + g * (G * LW);
+                if constexpr (G * LW == 2 && LSTR % 2 == 0) {
+                    *reinterpret_cast<uint2*>(dst) = make_uint2(ow[0], ow[1]);
+                } else if constexpr (G * LW % 4 == 0 && LSTR % 4 == 0) {
+#pragma unroll
+                    for (int k = 0; k < G * LW; k += 4)
+                        *reinterpret_cast<uint4*>(dst + k) = make_uint4(ow[k], ow[k + 1], ow[k + 2], ow[k + 3]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < G * LW; ++k) dst[k] = ow[k];
+                }
             }
         }
     };
 
     const int lg = lane & (W - 1), grp = lane / W;
     const bool head = edge && (p.edges[e].flags & EDGE_HEAD);
-    const int t0r = edge ? p.edges[e].t0r : p.L;     // rows below t0r are never traced
     int flip[V];
     init_flips<CF>(flip, lg, std::make_integer_sequence<int, V>{});
 
@@ -558,7 +575,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     for (int k = 0; k < S; ++k)
         pm[k] = head ? ((lg == 0 && k == 0) ? 0u : uint32_t(S_HEAD) * 0x00010001u) : 0u;
 
-    uint32_t* drow = decs + size_t(lane) * CF::WPS;     // + s*ROW
     uint32_t* gdec = nullptr;
     if (!edge) {
         gdec = p.dec + size_t(gw) * size_t(p.span_int) * ROW;
@@ -588,15 +604,15 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         } else {
             cp_async_wait<0>();
         }
-        if (c > 0) {
-            if (lane == 0) bulk_wait_read<0>();     // survivor buffer free again
-        }
         __syncwarp();
         if (next && p.P != 1) {
             depuncture(c + 1);
             __syncwarp();
         }
-        const uint32_t* lamrow = lam + size_t(c & 1) * T * PPW * XYW + size_t(edge ? 0 : grp) * XYW;
+        const uint32_t* lamrow = lam + size_t(c & 1) * PPW * LSTR + size_t(edge ? 0 : grp) * LSTR;
+        // survivor rows of this chunk, this lane's WPS words (direct stores:
+        // each warp writes 32 * WPS contiguous words per stage)
+        uint32_t* drow = gdec + size_t(c) * T * ROW + size_t(lane) * CF::WPS;
         if (nst == T) {
 #pragma unroll 1
             for (int j = 0; j < CF::NCYC; ++j) {
@@ -628,20 +644,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         for (int o = 1; o < W; o <<= 1) mn = __vmins2(mn, __shfl_xor_sync(0xffffffffu, mn, o));
 #pragma unroll
         for (int k = 0; k < S; ++k) pm[k] -= mn;
-        // stream this chunk's traced rows (>= t0r) to HBM: one bulk copy
-        const int r0 = max(c * T, t0r), r1 = c * T + nst;
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0 && r1 > r0) {
-#if PBVD_L2_HINTS
-            bulk_s2g_hint(gdec + size_t(r0) * ROW, smem_u32(decs + size_t(r0 - c * T) * ROW),
-                          uint32_t(r1 - r0) * ROW * 4u, policy_evict_last());
-#else
-            bulk_s2g(gdec + size_t(r0) * ROW, smem_u32(decs + size_t(r0 - c * T) * ROW),
-                     uint32_t(r1 - r0) * ROW * 4u);
-#endif
-            bulk_commit();
-        }
+        __syncwarp();      // every lane is done with lam[c & 1] before chunk c+2's transform
     }
 
     // ---- traceback start: min PM, lowest logical state on ties --------
@@ -668,7 +671,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             p.start_edge[e] = (p.edges[e].flags & EDGE_START0) ? 0 : int32_t(kA & 0xffu);
         }
     }
-    if (lane == 0) bulk_wait<0>();
     pdl_launch_dependents();   // the traceback grid may start scheduling
 }
 
