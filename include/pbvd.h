@@ -139,6 +139,15 @@ int pbvd_decode_host(pbvd_t h, const int8_t *h_llr_window, int64_t window_stage0
 int pbvd_set_lanes(pbvd_t h, int lanes);
 int pbvd_get_lanes(pbvd_t h);
 
+/* Kernel structure (default 1).  fused = 1: ONE kernel per launch group --
+ * every forward warp traces back its own blocks right after its forward
+ * pass (survivors re-read from L2 into the warp's shared memory).  fused = 0:
+ * the paper's two kernels "with different parallelism" (Alg. 1 K1 + K2,
+ * P:112): forward, then a traceback kernel with one thread per block.
+ * Both produce identical bits.  Returns PBVD_EINVAL for a NULL handle. */
+int pbvd_set_fused(pbvd_t h, int fused);
+int pbvd_get_fused(pbvd_t h);
+
 /* Upper bound on the survivor workspace in bytes (default 4 GiB); decodes
  * larger than one workspace run in waves. */
 int pbvd_set_workspace_limit(pbvd_t h, size_t bytes);

@@ -15,6 +15,7 @@ PBVD_TERMINATED = 1
 EXPORTS = (
     "pbvd_create", "pbvd_destroy", "pbvd_llr_count", "pbvd_stage_count", "pbvd_block_count",
     "pbvd_decode", "pbvd_decode_blocks", "pbvd_decode_host", "pbvd_set_lanes", "pbvd_get_lanes",
+    "pbvd_set_fused", "pbvd_get_fused",
     "pbvd_set_workspace_limit", "pbvd_set_profiling", "pbvd_kernel_times", "pbvd_get_info",
     "pbvd_supported", "pbvd_strerror", "pbvd_last_error", "pbvd_probe_acs_peak",
 )
@@ -61,6 +62,10 @@ def load(path: os.PathLike | None = None):
     L.pbvd_set_lanes.restype = i32
     L.pbvd_get_lanes.argtypes = [h]
     L.pbvd_get_lanes.restype = i32
+    L.pbvd_set_fused.argtypes = [h, i32]
+    L.pbvd_set_fused.restype = i32
+    L.pbvd_get_fused.argtypes = [h]
+    L.pbvd_get_fused.restype = i32
     L.pbvd_set_workspace_limit.argtypes = [h, ctypes.c_size_t]
     L.pbvd_set_workspace_limit.restype = i32
     L.pbvd_set_profiling.argtypes = [h, i32]

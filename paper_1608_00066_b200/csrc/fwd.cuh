@@ -48,6 +48,7 @@
 #include <utility>
 #include "params.h"
 #include "ptx.cuh"
+#include "tb.cuh"
 
 namespace pbvd {
 
@@ -67,9 +68,6 @@ struct Code {
     static constexpr bool symmetric = (gK == ALL) && (g0 == ALL);
 };
 
-__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
-__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
-__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 template <class C, int W_>
 struct Cfg {
@@ -390,7 +388,7 @@ __device__ __forceinline__ int64_t kept_before(const FwdParams& p, int64_t s, in
     return (s / p.P) * p.kp + p.cum[s % p.P];
 }
 
-template <class CF>
+template <class CF, bool FUSED>
 __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(const __grid_constant__ FwdParams p) {
     constexpr int V = CF::V, N = CF::N, S = CF::S, W = CF::W, R = CF::R, T = CF::T;
     constexpr int BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW, RAWB = CF::RAWB;
@@ -661,6 +659,30 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     for (int o = 1; o < W; o <<= 1) {
         kA = min(kA, __shfl_xor_sync(0xffffffffu, kA, o));
         kB = min(kB, __shfl_xor_sync(0xffffffffu, kB, o));
+    }
+    if constexpr (FUSED) {
+        // traceback of this warp's blocks, lane i = block i (+32, +64 ...)
+        constexpr int NBL = TbwCfg<CF>::NBL;
+        uint32_t stv[NBL];
+        int64_t ob[NBL];
+#pragma unroll
+        for (int m = 0; m < NBL; ++m) {
+            const int i = min(lane + 32 * m, BPW - 1);
+            const int src = (i >> 1) * W;
+            const uint32_t a = __shfl_sync(0xffffffffu, kA, src);
+            const uint32_t b = __shfl_sync(0xffffffffu, kB, src);
+            stv[m] = ((i & 1) ? b : a) & 0xffu;
+            ob[m] = p.out_bit0 + (wb0 + lane + 32 * m) * int64_t(p.D);
+        }
+        if (edge) {
+            stv[0] = (p.edges[e].flags & EDGE_START0) ? 0u : (__shfl_sync(0xffffffffu, kA, 0) & 0xffu);
+            ob[0] = p.edges[e].out_bit0;
+        }
+        const int nblk_tb = edge ? 1 : int(min(int64_t(BPW), int64_t(p.n_int) - wb0));
+        warp_traceback<CF>(wbase, gdec, span, edge ? p.edges[e].t0r : p.t0r,
+                           edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,
+                           !edge && p.word_out, p.out, lane);
+        return;
     }
     if (lg == 0) {
         if (!edge) {

@@ -7,16 +7,28 @@
 namespace pbvd {
 
 template <class CF>
+constexpr size_t fused_smem() {
+    return CF::SMEM > TbwCfg<CF>::SMEM ? CF::SMEM : ((TbwCfg<CF>::SMEM + 127) / 128) * 128;
+}
+template <class CF>
 cudaError_t prepare_cf() {
-    cudaError_t e = cudaFuncSetAttribute(fwd_kernel<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(CF::SMEM));
+    cudaError_t e = cudaFuncSetAttribute(fwd_kernel<CF, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fwd_kernel<CF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(fused_smem<CF>()));
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(tb_kernel<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(TbCfg<CF>::SMEM));
 }
 template <class CF>
 void launch_fwd(int grid, cudaStream_t s, const FwdParams& p) {
-    fwd_kernel<CF><<<grid, CF::NT, CF::SMEM, s>>>(p);
+    fwd_kernel<CF, false><<<grid, CF::NT, CF::SMEM, s>>>(p);
+}
+// forward + in-warp traceback in one kernel (warp_traceback, tb.cuh)
+template <class CF>
+void launch_fused(int grid, cudaStream_t s, const FwdParams& p) {
+    fwd_kernel<CF, true><<<grid, CF::NT, fused_smem<CF>(), s>>>(p);
 }
 // The traceback is launched with programmatic stream serialization (PDL):
 // its CTAs may be scheduled as soon as every forward CTA has signalled
@@ -57,10 +69,12 @@ Variant make_variant(int rank) {
     v.TT = TbCfg<CF>::TT;
     v.smem_fwd = CF::SMEM;
     v.smem_tb = TbCfg<CF>::SMEM;
+    v.smem_fused = fused_smem<CF>();
     v.default_rank = rank;
     v.prepare = &prepare_cf<CF>;
     v.fwd = &launch_fwd<CF>;
     v.tb = &launch_tb<CF>;
+    v.fused = &launch_fused<CF>;
     return v;
 }
 

@@ -5,6 +5,10 @@
 
 namespace pbvd {
 
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
 constexpr int MAX_EDGE = 32;      // edge blocks per launch (more -> extra launches)
 constexpr int S_HEAD = 8192;      // known-start sentinel, > v*128*R (reading c-12)
 
@@ -41,6 +45,11 @@ struct FwdParams {
     int32_t* start_edge;   // edge start states
     int span_edge_max;     // stage capacity of one edge region
     int n_edge;
+    // fused traceback (fwd_kernel<CF, true>): decoded bits go straight to out
+    uint8_t* out;
+    int64_t out_bit0;      // bit offset of the first interior block in out
+    int t0r, t1r;          // interior decoding range relative to lo (L, L+D)
+    int word_out;          // 1: interior blocks store aligned 32-bit words
     EdgeDesc edges[MAX_EDGE];
 };
 

@@ -69,6 +69,7 @@ struct pbvd_s {
     size_t ws_limit = size_t(4) << 30;
     std::vector<HostLane> lanes;
     bool prof = false;
+    bool fused = true;     // forward + in-warp traceback in one kernel (pbvd_set_fused)
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_fwd, ev_tb;   // indices into ev_pool
     int launches = 0;
@@ -244,6 +245,9 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     fp.dec_edge = dec_edge;
     fp.start_edge = start_edge;
     fp.span_edge_max = span_edge_max;
+    fp.out = out;
+    fp.t0r = int(L);
+    fp.t1r = int(L + D);
 
     TbParams tp{};
     tp.dec = dec_int;
@@ -334,26 +338,33 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         tp.n_int = fp.n_int;
         tp.n_int_ctas = int((cnt + 127) / 128);
         tp.out_bit0 = (g.i0 - B0) * D;
+        fp.out_bit0 = tp.out_bit0;
+        fp.word_out = tp.word_out;
         tp.n_edge = ne;
         for (int i = 0; i < ne; ++i) {
             fp.edges[i] = g.edges[size_t(i)];
             tp.edges[i] = g.edges[size_t(i)];
         }
+        const int fgrid = int((fp.n_int_warps + ne + v->NT / 32 - 1) / (v->NT / 32));
         const int ev = record(h, stream);
         if (ev >= 0) cudaEventRecord(h->ev_pool[ev], stream);
-        v->fwd(int((fp.n_int_warps + ne + v->NT / 32 - 1) / (v->NT / 32)), stream, fp);
+        if (h->fused) v->fused(fgrid, stream, fp);
+        else v->fwd(fgrid, stream, fp);
         if (ev >= 0) {
             cudaEventRecord(h->ev_pool[ev + 1], stream);
             h->ev_fwd.push_back({ev, ev + 1});
         }
-        const int ev2 = record(h, stream);
-        if (ev2 >= 0) cudaEventRecord(h->ev_pool[ev2], stream);
-        v->tb(tp.n_int_ctas + ne, stream, tp);
-        if (ev2 >= 0) {
-            cudaEventRecord(h->ev_pool[ev2 + 1], stream);
-            h->ev_tb.push_back({ev2, ev2 + 1});
+        h->launches += 1;
+        if (!h->fused) {
+            const int ev2 = record(h, stream);
+            if (ev2 >= 0) cudaEventRecord(h->ev_pool[ev2], stream);
+            v->tb(tp.n_int_ctas + ne, stream, tp);
+            if (ev2 >= 0) {
+                cudaEventRecord(h->ev_pool[ev2 + 1], stream);
+                h->ev_tb.push_back({ev2, ev2 + 1});
+            }
+            h->launches += 1;
         }
-        h->launches += 2;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
     }
@@ -572,6 +583,14 @@ int pbvd_set_lanes(pbvd_t h, int lanes) {
 }
 
 int pbvd_get_lanes(pbvd_t h) { return h ? h->var->W : PBVD_EINVAL; }
+
+int pbvd_set_fused(pbvd_t h, int fused) {
+    if (!h) return PBVD_EINVAL;
+    h->fused = fused != 0;
+    return PBVD_OK;
+}
+
+int pbvd_get_fused(pbvd_t h) { return h ? int(h->fused) : PBVD_EINVAL; }
 
 int pbvd_set_workspace_limit(pbvd_t h, size_t bytes) {
     if (!h || bytes < (size_t(1) << 20)) return PBVD_EINVAL;

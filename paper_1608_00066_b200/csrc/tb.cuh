@@ -27,6 +27,7 @@
 // ahead, so the dependent chain per step is a select and a shift.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include "params.h"
 #include "ptx.cuh"
 
@@ -129,6 +130,85 @@ __device__ __forceinline__ void tb_cycle(TbState& t, const uint32_t*& row,
     if (eb >= 0 && (w << 5) > ea && w < nwords)
         out32[word0 + w] = uint32_t(t.acc64 >> ((w << 5) - ea - 1));
     t.e = ea;
+}
+
+// ---- compact walk (N <= 64, or one survivor word per pair) -----------------
+// The survivor bits of ONE block at one stage form a small bit vector whose
+// bit q is the survivor bit of physical slot q: for N = 64 the pair's four
+// words (one 16-byte load shared by both lanes of the pair) halved by two
+// PRMTs into a uint64; for one word per pair the word itself, indexed by
+// tb_bitpos.  The load does not depend on the walk, so the dependent chain
+// per step is only shift -> and -> bit insert.
+template <class CF>
+__host__ __device__ constexpr bool tb_compact() { return CF::N == 64 || CF::W * CF::WPS == 1; }
+template <class CF>
+using RowT = typename std::conditional<CF::N == 64, uint64_t, uint32_t>::type;
+
+template <class CF>
+__device__ __forceinline__ RowT<CF> row_bits(const uint32_t* row, int woff, uint32_t sel) {
+    if constexpr (CF::N == 64) {
+        const uint4 w = *reinterpret_cast<const uint4*>(row + woff);
+        return (uint64_t(prmt(w.z, w.w, sel)) << 32) | prmt(w.x, w.y, sel);
+    } else {
+        return row[woff];
+    }
+}
+template <class CF>
+__device__ __forceinline__ uint32_t row_bit(RowT<CF> b, uint32_t q, uint32_t hbit) {
+    if constexpr (CF::N == 64) return uint32_t(b >> q) & 1u;
+    else return (b >> tb_bitpos<CF>(q, hbit)) & 1u;
+}
+template <class CF, int PH>
+__device__ __forceinline__ void tbc_steps(TbState& t, const uint32_t* row, int woff, uint32_t sel,
+                                          uint32_t hbit) {
+    const RowT<CF> b = row_bits<CF>(row, woff, sel);
+    const uint32_t dec = row_bit<CF>(b, t.q, hbit);
+    t.acc64 = (t.acc64 << 1) | dec;
+    t.q = (t.q & ~(1u << PH)) | (dec << PH);
+    if constexpr (PH > 0) tbc_steps<CF, PH - 1>(t, row - CF::ROW, woff, sel, hbit);
+}
+// v steps from row `row` (phase v-1) down, then the output word if complete
+template <class CF>
+__device__ __forceinline__ void tbc_cycle(TbState& t, const uint32_t* row, int woff, uint32_t sel,
+                                          uint32_t hbit, uint32_t* out32, int64_t word0,
+                                          int nwords) {
+    tbc_steps<CF, CF::V - 1>(t, row, woff, sel, hbit);
+    const int eb = t.e, ea = t.e - CF::V;
+    const int w = eb >> 5;
+    if (eb >= 0 && (w << 5) > ea && w < nwords)
+        out32[word0 + w] = uint32_t(t.acc64 >> ((w << 5) - ea - 1));
+    t.e = ea;
+}
+template <class CF>
+__device__ __forceinline__ void tbc_step_rt(TbState& t, int ph, const uint32_t* row, int woff,
+                                            uint32_t sel, uint32_t hbit, uint32_t* out32,
+                                            int64_t word0, int nwords) {
+    const RowT<CF> b = row_bits<CF>(row, woff, sel);
+    const uint32_t dec = row_bit<CF>(b, t.q, hbit);
+    t.acc64 = (t.acc64 << 1) | dec;
+    if ((t.e & 31) == 0 && t.e >= 0 && (t.e >> 5) < nwords)
+        out32[word0 + (t.e >> 5)] = uint32_t(t.acc64);
+    --t.e;
+    t.q = (t.q & ~(1u << ph)) | (dec << ph);
+}
+// one chunk [lo, hi) of the compact walk; rows(r) = ring row of stage r
+template <class CF, int TT, class RowFn>
+__device__ __forceinline__ void tbc_chunk(TbState& t, int lo, int hi, int c, RowFn rows, int woff,
+                                          uint32_t sel, uint32_t hbit, uint32_t* out32,
+                                          int64_t word0, int nwords) {
+    constexpr int V = CF::V;
+    if (hi - lo == TT && lo == c * TT) {
+        const uint32_t* row = rows(hi - 1);
+#pragma unroll 1
+        for (int cy = 0; cy < TT / V; ++cy)
+            tbc_cycle<CF>(t, row - cy * V * CF::ROW, woff, sel, hbit, out32, word0, nwords);
+    } else {
+        int ph = (hi - 1) % V;
+        for (int s = hi - 1; s >= lo; --s) {
+            tbc_step_rt<CF>(t, ph, rows(s), woff, sel, hbit, out32, word0, nwords);
+            ph = (ph == 0) ? V - 1 : ph - 1;
+        }
+    }
 }
 
 template <class CF>
@@ -294,6 +374,20 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
         return;
     }
 
+    if constexpr (tb_compact<CF>()) {
+        const uint32_t sel = h ? 0x7632u : 0x5410u;
+        for (int k = 0; k < nchunks; ++k) {
+            if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
+            wait(k);
+            int lo, hi;
+            chunk_rows(k, lo, hi);
+            if (active)
+                tbc_chunk<CF, TT>(t, lo, hi, c_top - k, [&](int r) { return slot_row(k, r); }, woff,
+                                  sel, hbit, out32, word0, nwords);
+            __syncthreads();      // slot k % NBUF free for chunk k + NBUF
+        }
+        return;
+    }
     for (int k = 0; k < nchunks; ++k) {
         // chunk k and k+1 resident (the walk looks one row ahead)
         if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
@@ -323,6 +417,198 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
             }
         }
         __syncthreads();          // slot k % NBUF free for chunk k + NBUF
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused traceback (fwd_kernel<CF, true>): the forward warp walks its own
+// blocks right after its forward pass -- one lane per block (NBL blocks per
+// lane when a warp holds more than 32) -- streaming its survivor region from
+// the top down through an NBUF-deep ring in the warp's (now free) shared
+// memory with cp.async.bulk + mbarrier, exactly as tb_kernel does per CTA.
+// The region was written by this warp moments earlier, so the rows come from
+// L2; while one warp walks (latency bound), the other warps of its SM
+// sub-partition keep the ALU pipes busy with their forward passes, and the
+// second launch and its grid-wide dependency disappear.
+template <class CF>
+struct TbwCfg {
+    static constexpr int NBUF = 3;
+#ifndef PBVD_FUSED_TT
+#define PBVD_FUSED_TT 18
+#endif
+    static constexpr int TT = CF::V * cmax(1, PBVD_FUSED_TT / CF::V);   // rows per chunk, multiple of v
+    static constexpr int NBL = (CF::BPW + 31) / 32;         // blocks per lane
+    static constexpr size_t RING = size_t(NBUF) * TT * CF::ROW * 4;
+    static constexpr size_t SMEM = RING + 64;
+    static constexpr int WSH = TbCfg<CF>::WSH;
+};
+
+template <class CF>
+__device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* region, int span,
+                                               int t0r, int t1r, int nblk,
+                                               const uint32_t (&st)[TbwCfg<CF>::NBL],
+                                               const int64_t (&obit)[TbwCfg<CF>::NBL], bool words,
+                                               uint8_t* out, int lane) {
+    using TC = TbwCfg<CF>;
+    constexpr int V = CF::V, W = CF::W, WPS = CF::WPS, ROW = CF::ROW;
+    constexpr int TT = TC::TT, NBUF = TC::NBUF, NBL = TC::NBL;
+    uint32_t* ring = reinterpret_cast<uint32_t*>(wsm);                 // [NBUF][TT][ROW]
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(wsm + TC::RING);
+
+    __syncwarp();              // every lane is done with the forward's shared memory
+    if (lane == 0) {
+        for (int b = 0; b < NBUF; ++b) mbar_init(smem_u32(&mbar[b]), 1);
+        fence_mbar_init();
+        fence_proxy_async_all();   // survivor stores (generic) before the bulk reads
+    }
+    __syncwarp();
+
+    const int s_min = min(span, t0r + V);
+    const int c_top = (span - 1) / TT;
+    const int c_bot = s_min / TT;
+    const int nchunks = (s_min < span) ? c_top - c_bot + 1 : 0;
+    auto chunk_rows = [&](int k, int& lo, int& hi) {
+        const int c = c_top - k;
+        lo = max(c * TT, s_min);
+        hi = min(c * TT + TT, span);
+    };
+    auto slot_row = [&](int k, int r) -> const uint32_t* {
+        const int c = c_top - k;
+        return ring + (size_t(k % NBUF) * TT + (r - c * TT)) * ROW;
+    };
+    auto issue = [&](int k) {
+        if (lane == 0) {
+            int lo, hi;
+            chunk_rows(k, lo, hi);
+            const uint32_t bytes = uint32_t(hi - lo) * ROW * 4u;
+            const uint32_t mb = smem_u32(&mbar[k % NBUF]);
+            mbar_arrive_expect_tx(mb, bytes);
+            bulk_g2s(smem_u32(slot_row(k, lo)), region + size_t(lo) * ROW, bytes, mb);
+        }
+    };
+    auto wait = [&](int k) { mbar_wait(smem_u32(&mbar[k % NBUF]), uint32_t(k / NBUF) & 1u); };
+
+    for (int k = 0; k < min(NBUF - 1, nchunks); ++k) issue(k);
+
+    const int pe = span % V;
+    const int nbits = t1r - t0r;
+    const int nwords = (nbits + 31) >> 5;
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
+    TbState t[NBL];
+    bool act[NBL];
+    int woff[NBL];
+    uint32_t hbit[NBL];
+#pragma unroll
+    for (int m = 0; m < NBL; ++m) {
+        const int i = lane + 32 * m;
+        act[m] = i < nblk;
+        woff[m] = (i >> 1) * W * WPS;
+        hbit[m] = 16u * uint32_t(i & 1);
+        t[m].q = ((st[m] << pe) | (st[m] >> (V - pe))) & uint32_t(CF::N - 1);
+        t[m].acc64 = 0;
+        for (int j = V - 1; j >= 0; --j)
+            t[m].acc64 = (t[m].acc64 << 1) | ((t[m].q >> ((span + j) % V)) & 1u);
+        t[m].acc = 0;
+        t[m].e = (span - 1) - t0r - V;
+        t[m].cnt = 0;
+        t[m].wcur = 0;
+    }
+
+    if (!words) {
+        // edge blocks / unaligned output: per-step walk with byte stores
+        int ph0 = (span - 1) % V;
+        uint32_t q[NBL], bacc[NBL];
+#pragma unroll
+        for (int m = 0; m < NBL; ++m) { q[m] = t[m].q; bacc[m] = 0; }
+        for (int k = 0; k < nchunks; ++k) {
+            if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
+            wait(k);
+            int lo, hi;
+            chunk_rows(k, lo, hi);
+#pragma unroll
+            for (int m = 0; m < NBL; ++m) {
+                if (!act[m]) continue;
+                int ph = ph0;
+                for (int s = hi - 1; s >= lo; --s) {
+                    const uint32_t* row = slot_row(k, s);
+                    const uint32_t wd = row[tb_word_index<CF>(q[m], woff[m])];
+                    const uint32_t dec = (wd >> tb_bitpos<CF>(q[m], hbit[m])) & 1u;
+                    if (s < t1r) {
+                        bacc[m] = (bacc[m] << 1) | ((q[m] >> ph) & 1u);
+                        const int eb = s - t0r;
+                        if ((eb & 7) == 0) out[(obit[m] + eb) >> 3] = uint8_t(bacc[m] & 0xffu);
+                    }
+                    q[m] = (q[m] & ~(1u << ph)) | (dec << ph);
+                    ph = (ph == 0) ? V - 1 : ph - 1;
+                }
+            }
+            ph0 = (ph0 - (hi - lo)) % V;
+            if (ph0 < 0) ph0 += V;
+            __syncwarp();
+        }
+#pragma unroll
+        for (int m = 0; m < NBL; ++m) {
+            if (!act[m]) continue;
+            int ph = ph0;
+            for (int s = s_min - 1; s >= t0r; --s) {
+                if (s < t1r) {
+                    bacc[m] = (bacc[m] << 1) | ((q[m] >> ph) & 1u);
+                    const int eb = s - t0r;
+                    if ((eb & 7) == 0) out[(obit[m] + eb) >> 3] = uint8_t(bacc[m] & 0xffu);
+                }
+                ph = (ph == 0) ? V - 1 : ph - 1;
+            }
+        }
+        return;
+    }
+
+    if constexpr (tb_compact<CF>()) {
+        for (int k = 0; k < nchunks; ++k) {
+            if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
+            wait(k);
+            int lo, hi;
+            chunk_rows(k, lo, hi);
+#pragma unroll
+            for (int m = 0; m < NBL; ++m) {
+                if (!act[m]) continue;
+                const uint32_t sel = hbit[m] ? 0x7632u : 0x5410u;
+                tbc_chunk<CF, TT>(t[m], lo, hi, c_top - k, [&](int r) { return slot_row(k, r); },
+                                  woff[m], sel, hbit[m], out32, obit[m] >> 5, nwords);
+            }
+            __syncwarp();          // slot k % NBUF free for chunk k + NBUF
+        }
+        return;
+    }
+    for (int k = 0; k < nchunks; ++k) {
+        if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
+        wait(k);
+        if (k + 1 < nchunks) wait(k + 1);
+        int lo, hi;
+        chunk_rows(k, lo, hi);
+        const int c = c_top - k;
+#pragma unroll
+        for (int m = 0; m < NBL; ++m) {
+            if (!act[m]) continue;
+            const int64_t word0 = obit[m] >> 5;
+            const uint32_t* row = slot_row(k, hi - 1);
+            if (k == 0) t[m].wcur = row[tb_word_index<CF>(t[m].q, woff[m])];
+            const uint32_t* below = (k + 1 < nchunks) ? slot_row(k + 1, lo - 1) : row;
+            if (hi - lo == TT && lo == c * TT) {
+#pragma unroll 1
+                for (int cy = 0; cy < TT / V - 1; ++cy)
+                    tb_cycle<CF>(t[m], row, row - V * ROW, woff[m], hbit[m], out32, word0, nwords);
+                tb_cycle<CF>(t[m], row, below, woff[m], hbit[m], out32, word0, nwords);
+            } else {
+                int ph = (hi - 1) % V;
+                for (int s = hi - 1; s >= lo; --s) {
+                    const uint32_t* nrow = (s > lo) ? row - ROW : below;
+                    tb_step_rt<CF>(t[m], ph, nrow, woff[m], hbit[m], out32, word0, nwords);
+                    row = nrow;
+                    ph = (ph == 0) ? V - 1 : ph - 1;
+                }
+            }
+        }
+        __syncwarp();          // slot k % NBUF free for chunk k + NBUF
     }
 }
 

@@ -17,11 +17,12 @@ struct Variant {
     int K, R, W;
     uint32_t polys[4];
     int BPC, BPW, NT, T, ROW, NR_TB, TT, BOXB;
-    size_t smem_fwd, smem_tb;
+    size_t smem_fwd, smem_tb, smem_fused;
     int default_rank;   // lower = preferred default for the code
     cudaError_t (*prepare)();
     void (*fwd)(int grid, cudaStream_t, const FwdParams&);
     void (*tb)(int grid, cudaStream_t, const TbParams&);
+    void (*fused)(int grid, cudaStream_t, const FwdParams&);
 };
 
 void add_variants_k3(std::vector<Variant>&);

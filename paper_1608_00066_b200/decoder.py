@@ -48,7 +48,7 @@ class Decoder:
     punct: None or an R x P keep matrix (rows in generator order)."""
 
     def __init__(self, K, polys, D, L, punct=None, soft_bits=8, terminated=True, device=0,
-                 lanes=0):
+                 lanes=0, fused=True):
         self._L = _lib.load()
         self.K, self.polys, self.D, self.L = int(K), tuple(int(p) for p in polys), int(D), int(L)
         self.R = len(self.polys)
@@ -70,6 +70,8 @@ class Decoder:
         self._h = h
         if lanes:
             self.set_lanes(lanes)
+        if not fused:
+            self.set_fused(False)
 
     # --------------------------------------------------------------- sizes
     def llr_count(self, n_info):
@@ -145,6 +147,15 @@ class Decoder:
     @property
     def lanes(self) -> int:
         return self._L.pbvd_get_lanes(self._h)
+
+    def set_fused(self, fused: bool):
+        """True: one kernel (forward + in-warp traceback); False: the paper's
+        two kernels (pbvd_set_fused)."""
+        _check(self._L.pbvd_set_fused(self._h, int(bool(fused))), self._h, "pbvd_set_fused")
+
+    @property
+    def fused(self) -> bool:
+        return bool(self._L.pbvd_get_fused(self._h))
 
     def set_workspace_limit(self, nbytes: int):
         _check(self._L.pbvd_set_workspace_limit(self._h, int(nbytes)), self._h,

@@ -26,9 +26,9 @@ def pbvd():
     return P
 
 
-def gpu_decode(P, code, llr, n_info, D, L, punct=None, terminated=True, lanes=0):
+def gpu_decode(P, code, llr, n_info, D, L, punct=None, terminated=True, lanes=0, fused=True):
     dec = P.Decoder(code["K"], code["polys"], D, L, punct=punct, terminated=terminated,
-                    lanes=lanes)
+                    lanes=lanes, fused=fused)
     d = llr.to("cuda") if not llr.is_cuda else llr
     out = dec.decode(d, n_info)
     torch.cuda.synchronize()
@@ -52,9 +52,10 @@ def test_golden_vectors_gpu(pbvd, orc, case):
     code = {"K": case["K"], "polys": tuple(int(p, 8) for p in case["polys_octal"])}
     llr = torch.tensor(case["llr"], dtype=torch.int8)
     for lanes in lane_variants(pbvd, code):
-        got, _ = gpu_decode(pbvd, code, llr, case["n_info"], case["D"], case["L"],
-                            case["punct"], case["terminated"], lanes)
-        assert got.tobytes().hex() == case["packed_hex"], lanes
+        for fused in (True, False):
+            got, _ = gpu_decode(pbvd, code, llr, case["n_info"], case["D"], case["L"],
+                                case["punct"], case["terminated"], lanes, fused)
+            assert got.tobytes().hex() == case["packed_hex"], (lanes, fused)
 
 
 SMALL = [
@@ -83,10 +84,12 @@ def test_small_streams_bit_exact(pbvd, orc, cfg):
     flags = orc.TERMINATED if term else 0
     want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, D, L, flags=flags, punct=punct))
     for lanes in lane_variants(pbvd, code):
-        got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, punct, term, lanes)
-        assert got.shape == want.shape
-        bad = np.nonzero(got != want)[0]
-        assert bad.size == 0, f"lanes={lanes}: {bad.size} bytes differ, first at {bad[:8]}"
+        for fused in (True, False):
+            got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, punct, term, lanes, fused)
+            assert got.shape == want.shape
+            bad = np.nonzero(got != want)[0]
+            assert bad.size == 0, (f"lanes={lanes} fused={fused}: {bad.size} bytes differ, "
+                                   f"first at {bad[:8]}")
 
 
 def test_saturated_and_extreme_inputs(pbvd, orc):
@@ -100,8 +103,9 @@ def test_saturated_and_extreme_inputs(pbvd, orc):
         llr = torch.tensor(arr.astype(np.int8))
         want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, D, L))
         for lanes in lane_variants(pbvd, code):
-            got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, lanes=lanes)
-            assert (got == want).all(), lanes
+            for fused in (True, False):
+                got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, lanes=lanes, fused=fused)
+                assert (got == want).all(), (lanes, fused)
 
 
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
@@ -111,10 +115,11 @@ def test_config_full_size_bit_exact(pbvd, orc, cfg):
     code, punct = synth.CODES[c["code"]], synth.PUNCT[c["punct"]]
     info, llr = synth.make_stream(code, c["n_info"], c["ebn0"], c["seed"], punct, c["hard"],
                                   device="cuda")
-    got, _ = gpu_decode(pbvd, code, llr, c["n_info"], c["D"], c["L"], punct)
     want = orc.pack_bits(orc.decode(code, llr.cpu().numpy(), c["n_info"], c["D"], c["L"],
                                     punct=punct))
-    assert (got == want).all()
+    for fused in (True, False):
+        got, _ = gpu_decode(pbvd, code, llr, c["n_info"], c["D"], c["L"], punct, fused=fused)
+        assert (got == want).all(), fused
     # and the decoder actually decodes: BER in the expected range
     ber = (unpack(got, c["n_info"]) != info.cpu().numpy()).mean()
     assert ber < (2e-2 if c["hard"] else 1e-4)
@@ -132,7 +137,8 @@ def test_compute_sanitizer_memcheck_clean(pbvd):
         pytest.skip("compute-sanitizer not available")
     root = Path(__file__).resolve().parents[1]
     for args in (["k7", "3000", "64", "20", "2"], ["k7", "2000", "96", "30", "4", "3/4"],
-                 ["k9", "1500", "64", "20", "8"]):
+                 ["k9", "1500", "64", "20", "8"], ["k7", "3000", "64", "20", "2", "1/2", "0"],
+                 ["k3", "3000", "64", "20", "1"]):
         r = subprocess.run([cs, "--tool", "memcheck", "--error-exitcode", "9", sys.executable,
                             str(root / "tools" / "debug_case.py"), *args],
                            capture_output=True, text=True, timeout=600, cwd=root)

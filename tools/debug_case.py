@@ -13,9 +13,10 @@ D = int(sys.argv[3]) if len(sys.argv) > 3 else 64
 L = int(sys.argv[4]) if len(sys.argv) > 4 else 20
 lanes = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 pk = sys.argv[6] if len(sys.argv) > 6 else "1/2"
+fused = (sys.argv[7] != "0") if len(sys.argv) > 7 else True
 code, punct = synth.CODES[name], synth.PUNCT[pk]
 info, llr = synth.make_stream(code, n_info, 3.0, 5, punct)
-dec = P.Decoder(code["K"], code["polys"], D, L, punct=punct, lanes=lanes)
+dec = P.Decoder(code["K"], code["polys"], D, L, punct=punct, lanes=lanes, fused=fused)
 got = dec.decode(llr.cuda(), n_info).cpu().numpy()
 torch.cuda.synchronize()
 want = O.pack_bits(O.decode(code, llr.numpy(), n_info, D, L, punct=punct))

@@ -44,6 +44,14 @@ __device__ __forceinline__ uint32_t op_vote(uint32_t a, uint32_t b, uint32_t c) 
         if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;                                   \
     }
 
+__device__ __forceinline__ uint32_t op_addc(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d; asm volatile("mad.lo.u32 %0, %1, 1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t op_addimm(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d; asm volatile("add.u32 %0, %1, 0x7fff7fff;" : "=r"(d) : "r"(a)); return d; }
+__device__ __forceinline__ uint32_t op_vadd2r(uint32_t a, uint32_t b, uint32_t c) { return __vadd2(a, b); }
+KERNEL(addc, op_addc)
+KERNEL(addimm, op_addimm)
+KERNEL(vadd2r, op_vadd2r)
 KERNEL(iadd3, op_iadd3)
 KERNEL(imad, op_imad)
 KERNEL(prmt, op_prmt)
@@ -82,6 +90,11 @@ MIX(mix_viaddmin_iadd3, op_viaddmin, op_iadd3)
 MIX(mix_prmt_imad, op_prmt, op_imad)
 MIX(mix_vote_viaddmin, op_vote, op_viaddmin)
 MIX(mix_vibmin_imad, op_vibmin, op_imad)
+MIX(mix_addc_addimm, op_addc, op_addimm)
+MIX(mix_viaddmin_addimm, op_viaddmin, op_addimm)
+MIX(mix_viaddmin_addc, op_viaddmin, op_addc)
+MIX(mix_imad_addimm, op_imad, op_addimm)
+MIX(mix_imad_addc, op_imad, op_addc)
 
 typedef void (*kfn)(uint32_t*, uint32_t, long long*);
 
@@ -89,6 +102,7 @@ int main() {
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     struct { const char* name; kfn f; int ops_per_chain_iter; } ks[] = {
+        {"mad a*1+b", k_addc, 1}, {"add a+imm", k_addimm, 1}, {"__vadd2 reg", k_vadd2r, 1},
         {"IADD3 (sub+add)", k_iadd3, 1}, {"IMAD (mad.lo reg)", k_imad, 1}, {"PRMT", k_prmt, 1},
         {"LOP3", k_lop3, 1}, {"VIADDMNMX.S16x2", k_viaddmin, 1}, {"VIMNMX.S16x2 (+LOP3)", k_vmin, 2},
         {"VIMNMX.S16x2 w/ preds (+SEL/IADD)", k_vibmin, 2}, {"VIADD.16x2 (+LOP3)", k_vadd2, 2},
@@ -96,6 +110,9 @@ int main() {
         {"mix VIADDMNMX|IMAD", k_mix_viaddmin_imad, 1}, {"mix IADD3|IMAD", k_mix_iadd3_imad, 1},
         {"mix VIADDMNMX|IADD3", k_mix_viaddmin_iadd3, 1}, {"mix PRMT|IMAD", k_mix_prmt_imad, 1},
         {"mix VOTE|VIADDMNMX", k_mix_vote_viaddmin, 1}, {"mix VIBMIN|IMAD", k_mix_vibmin_imad, 1},
+        {"mix mad1|a+imm", k_mix_addc_addimm, 1}, {"mix VIADDMNMX|a+imm", k_mix_viaddmin_addimm, 1},
+        {"mix VIADDMNMX|mad1", k_mix_viaddmin_addc, 1}, {"mix IMAD|a+imm", k_mix_imad_addimm, 1},
+        {"mix IMAD|mad1", k_mix_imad_addc, 1},
     };
     uint32_t* out; long long* cyc;
     cudaMalloc(&out, 4096); cudaMalloc(&cyc, sizeof(long long) * nsm * 64);

@@ -11,8 +11,10 @@ c = synth.CONFIGS[cfg]
 code, punct = synth.CODES[c["code"]], synth.PUNCT[c["punct"]]
 n_info = int(sys.argv[2]) if len(sys.argv) > 2 else c["n_info"]
 info, llr = synth.make_stream(code, n_info, c["ebn0"], c["seed"], punct, c["hard"], device="cuda")
-for lanes in sorted({l for (K, R, p, l) in P.supported() if K == code["K"] and tuple(p) == tuple(code["polys"])}):
-    dec = P.Decoder(code["K"], code["polys"], c["D"], c["L"], punct=punct, lanes=lanes)
+import os, itertools
+lanes_all = sorted({l for (K, R, p, l) in P.supported() if K == code["K"] and tuple(p) == tuple(code["polys"])})
+for fused, lanes in itertools.product([int(x) for x in os.environ.get("QT_FUSED", "1").split()], lanes_all):
+    dec = P.Decoder(code["K"], code["polys"], c["D"], c["L"], punct=punct, lanes=lanes, fused=bool(fused))
     dec.set_profiling(True)
     out = dec.decode(llr, n_info)
     torch.cuda.synchronize()
@@ -32,4 +34,4 @@ for lanes in sorted({l for (K, R, p, l) in P.supported() if K == code["K"] and t
         ts2.append(e0.elapsed_time(e1))
     ts2.sort()
     ms2 = ts2[len(ts2)//2]
-    print(f"{cfg} n_info={n_info} lanes={lanes}: {ms:.3f} ms  {n_info/ms/1e6:.2f} Gb/s  fwd {fw[5]:.3f} ms tb {tb[5]:.3f} ms  launches={n}  | no-prof {ms2:.3f} ms {n_info/ms2/1e6:.2f} Gb/s", flush=True)
+    print(f"{cfg} n_info={n_info} lanes={lanes} fused={fused}: {ms:.3f} ms  {n_info/ms/1e6:.2f} Gb/s  fwd {fw[5]:.3f} ms tb {tb[5]:.3f} ms  launches={n}  | no-prof {ms2:.3f} ms {n_info/ms2/1e6:.2f} Gb/s", flush=True)
