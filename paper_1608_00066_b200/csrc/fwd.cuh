@@ -50,6 +50,23 @@
 #include "ptx.cuh"
 #include "tb.cuh"
 
+// compile-time experiment switches (defaults are the measured best)
+#ifndef PBVD_L2_HINTS
+#define PBVD_L2_HINTS 0
+#endif
+#ifndef PBVD_DEC_HINT
+#define PBVD_DEC_HINT 1
+#endif
+#ifndef PBVD_IN_HINT
+#define PBVD_IN_HINT 0
+#endif
+#ifndef PBVD_PACK_TREE
+#define PBVD_PACK_TREE 0
+#endif
+#ifndef PBVD_FMA_SPLIT
+#define PBVD_FMA_SPLIT 1
+#endif
+
 namespace pbvd {
 
 template <int K_, int R_, uint32_t G0, uint32_t G1, uint32_t G2 = 0, uint32_t G3 = 0>
@@ -253,6 +270,20 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
         }
         words[0] = (wd ^ inv) & (0x01010101u * ((1u << H) - 1u));
     }
+#if PBVD_DEC_HINT
+    // survivor stores with an L2 eviction-priority hint (the fused traceback
+    // re-reads them from L2)
+    const uint64_t pol = PBVD_DEC_HINT == 1 ? policy_evict_last_nv() : policy_evict_first_nv();
+    if constexpr (WPS == 1) {
+        st_global_hint(drow, words[0], pol);
+    } else if constexpr (WPS == 2) {
+        st_global_v2_hint(drow, words[0], words[1], pol);
+    } else {
+#pragma unroll
+        for (int i = 0; i < WPS; i += 4)
+            st_global_v4_hint(drow + i, words[i], words[i + 1], words[i + 2], words[i + 3], pol);
+    }
+#else
     if constexpr (WPS == 1) {
         drow[0] = words[0];
     } else if constexpr (WPS == 2) {
@@ -263,6 +294,7 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
             *reinterpret_cast<uint4*>(drow + i) =
                 make_uint4(words[i], words[i + 1], words[i + 2], words[i + 3]);
     }
+#endif
 }
 
 // One trellis stage at compile-time phase P (Eq. 1 per output state).
@@ -270,15 +302,6 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
 // IADD3 (ALU pipe) for outputs with FMA_OUT(k) false, and two IMADs (FMA
 // pipe: E + (BM_own + C), then - m_other) otherwise, so the ALU pipe --
 // which also carries VIADDMNMX, PRMT and LOP3 -- is not the only one busy.
-#ifndef PBVD_L2_HINTS
-#define PBVD_L2_HINTS 0
-#endif
-#ifndef PBVD_PACK_TREE
-#define PBVD_PACK_TREE 0
-#endif
-#ifndef PBVD_FMA_SPLIT
-#define PBVD_FMA_SPLIT 1
-#endif
 template <class CF>
 __host__ __device__ constexpr bool fma_out(int k) {
     return PBVD_FMA_SPLIT == 0 ? false : PBVD_FMA_SPLIT == 1 ? (k & 1) != 0 : (k % 3) != 0;
@@ -439,9 +462,16 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             woffs[(c & 1) * BPW + i] = uint8_t((vlo + uintptr_t(k0)) & 15);
             if (ga >= vlo && ga + RAWB <= vhi) {
                 // interior fast path: a fixed number of 16-byte vectors
+#if PBVD_IN_HINT
+                const uint64_t ipol = policy_evict_first_nv();
+#pragma unroll
+                for (int j = 0; j < RAWB / 16; ++j)
+                    cp_async16_hint(smem_u32(dst + 16 * j), reinterpret_cast<const void*>(ga + 16 * j), ipol);
+#else
 #pragma unroll
                 for (int j = 0; j < RAWB / 16; ++j)
                     cp_async16(smem_u32(dst + 16 * j), reinterpret_cast<const void*>(ga + 16 * j));
+#endif
             } else {
                 const int64_t k1 = kept_before(p, a + max(nst, 0), R) - p.kb_ws0;
                 const uintptr_t gb = (vlo + uintptr_t(k1) + 15) & ~uintptr_t(15);

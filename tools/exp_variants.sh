@@ -3,6 +3,6 @@
 for v in "$@"; do
   PBVD_NVCC_EXTRA="$v" python -m paper_1608_00066_b200.build --force > /dev/null || exit 1
   echo "== $v"
-  for c in ${CONFIGS:-C2}; do python tools/quick_time.py $c 2>&1 | grep Gb/s | grep -v "lanes=1"; done
+  for c in ${CONFIGS:-C2}; do python tools/quick_time.py $c 2>&1 | grep Gb/s | grep "lanes=2"; done
 done
 python -m paper_1608_00066_b200.build --force > /dev/null
