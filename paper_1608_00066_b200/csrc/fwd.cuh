@@ -709,6 +709,9 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             ob[0] = p.edges[e].out_bit0;
         }
         const int nblk_tb = edge ? 1 : int(min(int64_t(BPW), int64_t(p.n_int) - wb0));
+#ifdef PBVD_EXP_NO_TB
+        if (nblk_tb > 0) return;     // timing experiment only: skip the walk
+#endif
         warp_traceback<CF>(wbase, gdec, span, edge ? p.edges[e].t0r : p.t0r,
                            edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,
                            !edge && p.word_out, p.out, lane);

@@ -113,6 +113,10 @@ __device__ __forceinline__ void bulk_g2s_hint(uint32_t sdst, const void* gsrc, u
         "[%0], [%1], %2, [%3], %4;"
         ::"r"(sdst), "l"(gsrc), "r"(bytes), "r"(mbar), "l"(policy) : "memory");
 }
+// L2 prefetch of a global range (no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

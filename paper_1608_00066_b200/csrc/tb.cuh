@@ -433,6 +433,9 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
 template <class CF>
 struct TbwCfg {
     static constexpr int NBUF = 3;
+#ifndef PBVD_TB_PREFETCH
+#define PBVD_TB_PREFETCH 0
+#endif
 #ifndef PBVD_FUSED_TT
 #define PBVD_FUSED_TT 18
 #endif
@@ -489,6 +492,17 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
     auto wait = [&](int k) { mbar_wait(smem_u32(&mbar[k % NBUF]), uint32_t(k / NBUF) & 1u); };
 
     for (int k = 0; k < min(NBUF - 1, nchunks); ++k) issue(k);
+#if PBVD_TB_PREFETCH
+    // every later chunk of the region goes in flight to L2 at once, so the
+    // ring's bulk copies hit L2 instead of waiting on HBM one chunk at a time
+    if (lane == 0) {
+        for (int k = NBUF - 1; k < nchunks; ++k) {
+            int lo, hi;
+            chunk_rows(k, lo, hi);
+            bulk_prefetch_l2(region + size_t(lo) * ROW, uint32_t(hi - lo) * ROW * 4u);
+        }
+    }
+#endif
 
     const int pe = span % V;
     const int nbits = t1r - t0r;

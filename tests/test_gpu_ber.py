@@ -1,0 +1,56 @@
+"""GPU BER harness checks (tools/ber_sweep.py): the
+decoder's error rate against the closed-form union bound of the (171,133)
+code, and the Fig. 4 trend (BER non-increasing in L)."""
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1608_00066_b200 import build
+    build.build()
+    import paper_1608_00066_b200 as P
+    return P
+
+
+def _tools():
+    import importlib.util
+    from pathlib import Path
+    p = Path(__file__).resolve().parents[1] / "tools" / "ber_sweep.py"
+    spec = importlib.util.spec_from_file_location("ber_sweep", p)
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+@pytest.mark.parametrize("ebn0,n_bits", [(4.0, 1 << 25), (4.5, 1 << 27), (5.0, 1 << 29)])
+def test_gpu_ber_within_union_bound_band(P, ebn0, n_bits):
+    """K=7 soft 8-bit BER at D=512, L=42 within [0.55, 1.25] x the union bound
+    (the bound is tight at these SNRs), with >= 150 errors per point."""
+    B = _tools()
+    errs, n = B.ber_point(P, synth.CODES["k7"], ebn0, 512, 42, n_bits, seed=900 + int(ebn0 * 10))
+    assert errs >= 150, errs
+    ratio = (errs / n) / B.union_bound_k7(ebn0)
+    assert 0.55 <= ratio <= 1.25, (errs, n, ratio)
+
+
+def test_gpu_ber_fig4_trend_in_L(P):
+    """Fig. 4: at fixed Eb/N0 the BER does not increase with the
+    overlap L and levels off (the min-PM start of reading c-10 converges by
+    L ~ 28); short L is measurably worse."""
+    B = _tools()
+    code = synth.CODES["k7"]
+    bers = []
+    for L in (7, 14, 28, 42, 63):
+        errs, n = B.ber_point(P, code, 3.0, 512, L, 1 << 24, seed=321)
+        bers.append(errs / n)
+    for a, b in zip(bers, bers[1:]):
+        assert b <= a * 1.15, bers          # non-increasing up to sampling noise
+    assert bers[0] > 1.2 * bers[-1], bers   # L = 7 is not converged
+    assert abs(bers[3] - bers[4]) <= 0.15 * bers[4], bers   # L = 42 ~ L = 63
