@@ -452,10 +452,32 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         same = bool(torch.equal(out_h, out.cpu()))
-        e2e = {"value": n_total / float(e2e_s.item()) / 1e9, "unit": UNIT,
+        # the PCIe bound of this step: plain pinned copies of the same bytes
+        # (H2D of the soft values, D2H of the bits; full duplex, so the
+        # slower direction bounds an ideally overlapped pipeline)
+        d_in = torch.empty_like(llr_h, device=dev)
+        d_out = torch.empty_like(out_h, device=dev)
+        ts_in, ts_out = [], []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            d_in.copy_(llr_h, non_blocking=True)
+            torch.cuda.synchronize()
+            ts_in.append(time.perf_counter() - t)
+            t = time.perf_counter()
+            out_h.copy_(d_out, non_blocking=True)
+            torch.cuda.synchronize()
+            ts_out.append(time.perf_counter() - t)
+        t_in, t_out = min(ts_in), min(ts_out)
+        e2e_v = n_total / float(e2e_s.item()) / 1e9
+        bound = n_total / max(t_in, t_out) / 1e9
+        e2e = {"value": e2e_v, "unit": UNIT,
                "h2d_bytes_per_step": int(llr_h.numel()), "d2h_bytes_per_step": int(out_h.numel()),
                "api": "pbvd_decode_host (pinned host buffers, 3 streams)",
-               "matches_device_path": same}
+               "matches_device_path": same,
+               "pcie": {"h2d_gbs": llr_h.numel() / t_in / 1e9, "d2h_gbs": out_h.numel() / t_out / 1e9,
+                        "bound_value": bound, "frac_of_bound": e2e_v / bound}}
+        del d_in, d_out
 
     # ---- CPU baseline: the oracle on this host (rank 0, N == 1) ------------
     cpu = None

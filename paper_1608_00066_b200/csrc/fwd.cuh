@@ -526,35 +526,46 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     // stage) are interleaved A/B, biased by +128 (u = lam ^ 0x80) and stored
     // as LW words to lam[c & 1][pair][stage].  One item = (pair, G stages) =
     // G*R/4 whole words per block, read as aligned words funnel-shifted to the
-    // window offset; consecutive lanes take consecutive groups of one pair
-    // (conflict-free reads and 8/16-byte stores).
+    // window offset.  Lane l always serves pair l % PPW (so its window bases
+    // and offsets are per-slice constants); the W lanes of a pair split the
+    // slice's GPS groups.
+    constexpr int GPS = (NG + CF::NCYC - 1) / CF::NCYC;     // groups per pair per slice
+    constexpr int TPER = (GPS + W - 1) / W;                 // items per lane per slice
+    const int tp = lane % PPW, tsub = lane / PPW;
     auto transform = [&](int c, int j) {
-        const int npair = edge ? 1 : PPW;
         const bool dense = (p.P == 1);            // else read the depunctured dep[]
+        if (edge && tp != 0) return;              // an edge unit has one (replicated) pair
         const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
         const uint8_t* wo = woffs + (c & 1) * BPW;
-        uint32_t* lb = lam + size_t(c & 1) * PPW * LSTR;
+        uint32_t* lb = lam + size_t(c & 1) * PPW * LSTR + size_t(tp) * LSTR;
         constexpr int GW = G * R / 4;                     // words per block per item
-        constexpr int NITEM = PPW * NG;
-        constexpr int PER = (NITEM + 32 * CF::NCYC - 1) / (32 * CF::NCYC);
+        const uint8_t* base[2];
+        int o0[2];
+        uint32_t sh[2];
 #pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int it = (j * PER + u) * 32 + lane;
-            const int pr0 = it / NG, g = it - (it / NG) * NG;
-            const bool valid = pr0 < npair;
-            const int pr = valid ? pr0 : 0;
+        for (int h = 0; h < 2; ++h) {
+            const int i = edge ? 0 : 2 * tp + h;
+            o0[h] = dense ? int(wo[i]) : 0;
+            base[h] = rb + size_t(i) * RAWB + (o0[h] & ~3);
+            sh[h] = uint32_t(o0[h] & 3) * 8u;
+        }
+#pragma unroll
+        for (int u = 0; u < TPER; ++u) {
+            // straight-line: an item past the slice is computed on a clamped
+            // group and not stored (no divergent branch inside the ACS loop)
+            const int gl = tsub + W * u;                  // group within the slice
+            const int g0 = j * GPS + gl;
+            const bool valid = gl < GPS && g0 < NG;
+            const int g = valid ? g0 : j * GPS;
             uint32_t v[2][GW];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int i = edge ? 0 : 2 * pr + h;
-                const int o = (dense ? int(wo[i]) : 0) + 4 * GW * g;
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB + (o & ~3));
-                const uint32_t sh = uint32_t(o & 3) * 8u;
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(base[h] + 4 * GW * g);
                 uint32_t wl = w[0];
 #pragma unroll
                 for (int k = 0; k < GW; ++k) {
                     const uint32_t wh = w[k + 1];
-                    v[h][k] = __funnelshift_r(wl, wh, sh) ^ 0x80808080u;   // u = lam + 128
+                    v[h][k] = __funnelshift_r(wl, wh, sh[h]) ^ 0x80808080u;   // u = lam + 128
                     wl = wh;
                 }
             }
@@ -577,18 +588,17 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                     }
                 }
             }
-            if (valid) {
-                uint32_t* dst = lb + size_t(pr) * LSTR + g * (G * LW);
-                if constexpr (G * LW == 2 && LSTR % 2 == 0) {
-                    *reinterpret_cast<uint2*>(dst) = make_uint2(ow[0], ow[1]);
-                } else if constexpr (G * LW % 4 == 0 && LSTR % 4 == 0) {
+            uint32_t* dst = lb + g * (G * LW);
+            if (!valid) continue;
+            if constexpr (G * LW == 2 && LSTR % 2 == 0) {
+                *reinterpret_cast<uint2*>(dst) = make_uint2(ow[0], ow[1]);
+            } else if constexpr (G * LW % 4 == 0 && LSTR % 4 == 0) {
 #pragma unroll
-                    for (int k = 0; k < G * LW; k += 4)
-                        *reinterpret_cast<uint4*>(dst + k) = make_uint4(ow[k], ow[k + 1], ow[k + 2], ow[k + 3]);
-                } else {
+                for (int k = 0; k < G * LW; k += 4)
+                    *reinterpret_cast<uint4*>(dst + k) = make_uint4(ow[k], ow[k + 1], ow[k + 2], ow[k + 3]);
+            } else {
 #pragma unroll
-                    for (int k = 0; k < G * LW; ++k) dst[k] = ow[k];
-                }
+                for (int k = 0; k < G * LW; ++k) dst[k] = ow[k];
             }
         }
     };
