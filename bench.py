@@ -322,6 +322,7 @@ def run_ours(args):
     # measured throughput of the all-ALU ACS sequence (pbvd_probe_acs_peak):
     # reported beside the derived roofline as a cross-check
     probe_acs, _ = P.probe_acs_peak(local)
+    probe_bal, _ = P.probe_acs_balanced(local)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -404,6 +405,7 @@ def run_ours(args):
                         f"ALU/FMA pipes at 0.5 and issue at 1 instr/cycle, "
                         f"{sol_f:.2f} of decision operands on FMA)"),
         "probe_all_alu_tacs": probe_acs / 1e12,
+        "probe_balanced_tacs": probe_bal / 1e12,
         "acs_per_launch": acs_step, "kernel_ms": fwd_ms, "tb_kernel_ms": tb_ms,
         "kernel_share_of_step": fwd_ms / ms_per_step,
         "hbm": {"algorithmic_bytes_per_launch": alg_bytes, "achieved_gbs": fwd_hbm_gbs,

@@ -175,6 +175,12 @@ int pbvd_get_info(pbvd_t h, pbvd_info *info);
  * block at one stage) and the best kernel time in ms.  Synchronous. */
 int pbvd_probe_acs_peak(int device, double *acs_per_s, double *ms);
 
+/* The same probe with the forward kernel's pipe balancing (every other
+ * decision operand formed by two IMADs on the FMA pipe): the measured ACS
+ * rate of the balanced minimal sequence, a cross-check of the derived
+ * roofline bench.py reports.  Same arguments/errors. */
+int pbvd_probe_acs_balanced(int device, double *acs_per_s, double *ms);
+
 /* Compiled (K, R, polys...) combinations, as text "K:R:o1,o2[,o3]:lanes;..." */
 const char *pbvd_supported(void);
 

@@ -18,6 +18,7 @@ EXPORTS = (
     "pbvd_set_fused", "pbvd_get_fused",
     "pbvd_set_workspace_limit", "pbvd_set_profiling", "pbvd_kernel_times", "pbvd_get_info",
     "pbvd_supported", "pbvd_strerror", "pbvd_last_error", "pbvd_probe_acs_peak",
+    "pbvd_probe_acs_balanced",
 )
 
 
@@ -78,6 +79,9 @@ def load(path: os.PathLike | None = None):
     L.pbvd_probe_acs_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double)]
     L.pbvd_probe_acs_peak.restype = i32
+    L.pbvd_probe_acs_balanced.argtypes = [i32, ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_double)]
+    L.pbvd_probe_acs_balanced.restype = i32
     L.pbvd_supported.argtypes = []
     L.pbvd_supported.restype = cp
     L.pbvd_strerror.argtypes = [i32]

@@ -51,6 +51,12 @@
 #include "tb.cuh"
 
 // compile-time experiment switches (defaults are the measured best)
+#ifndef PBVD_SKIP_ROWS
+#define PBVD_SKIP_ROWS 0
+#endif
+#ifndef PBVD_MAXREG
+#define PBVD_MAXREG 200
+#endif
 #ifndef PBVD_L2_HINTS
 #define PBVD_L2_HINTS 0
 #endif
@@ -98,7 +104,7 @@ struct Cfg {
     static constexpr int BPW = 2 * PPW;       // blocks per warp (= per survivor region)
     static constexpr int NWARP = 1;            // warps per CTA (each warp is autonomous)
     static constexpr int NT = NWARP * 32;
-    static constexpr int MAXREG = 200;         // room for the unrolled stage state
+    static constexpr int MAXREG = PBVD_MAXREG;  // room for the unrolled stage state
     static constexpr int BPC = NWARP * BPW;   // blocks per CTA
     static constexpr int PPC = NWARP * PPW;   // pairs per CTA
     static constexpr int T = V * (32 / V);    // stages per chunk = normalisation period
@@ -221,7 +227,7 @@ __device__ __forceinline__ void bm_vector(const XY<CF>& xy, int flip, uint32_t (
 // bit = 16*h + 8*(q_reg / (S/2)) + q_reg % (S/2)         (S < 16).
 template <class CF>
 __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t inv,
-                                           uint32_t* drow) {
+                                           uint32_t* drow, bool st) {
     constexpr int S = CF::S, WPS = CF::WPS;
     constexpr uint32_t SEL = 0xFBD9u;   // [sgn a.b1, sgn b.b1, sgn a.b3, sgn b.b3]
     uint32_t words[WPS];
@@ -270,6 +276,7 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
         }
         words[0] = (wd ^ inv) & (0x01010101u * ((1u << H) - 1u));
     }
+    if (!st) return;       // a row the traceback never reads (below its first row)
 #if PBVD_DEC_HINT
     // survivor stores with an L2 eviction-priority hint (the fused traceback
     // re-reads them from L2)
@@ -309,7 +316,8 @@ __host__ __device__ constexpr bool fma_out(int k) {
 
 template <class CF, int P>
 __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
-                                          int lg, uint32_t* drow, uint32_t one, uint32_t neg1) {
+                                          int lg, uint32_t* drow, bool st, uint32_t one,
+                                          uint32_t neg1) {
     using C = typename CF::code;
     constexpr int S = CF::S, NC = CF::NC;
     constexpr int g0 = C::g0, gK = C::gK;
@@ -341,7 +349,7 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             t[k] = tE;
             t[k | pb] = tO;
         }
-        pack_store<CF>(t, 0u, drow);
+        pack_store<CF>(t, 0u, drow, st);
     } else {
         // ---- butterfly partner in lane lg ^ (1 << li) ----------------------
         constexpr int li = P - CF::LB;
@@ -373,7 +381,7 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             if (fma_out<CF>(k)) t[k] = imad(mR, neg1, imad(own, one, PCo[a]));
             else t[k] = sub_add(own, mR, PCo[a]);
         }
-        pack_store<CF>(t, 0u - lb, drow);
+        pack_store<CF>(t, 0u - lb, drow, st);
     }
 }
 
@@ -384,17 +392,19 @@ template <class CF, int P, bool FULL>
 struct Cycle {
     static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const uint32_t* lamrow,
                                                const int (&flip)[CF::V], int lg, uint32_t* drow,
-                                               int s0, int nst, const XY<CF>& cur, uint32_t one,
-                                               uint32_t neg1) {
+                                               int s0, int nst, int st_lo, const XY<CF>& cur,
+                                               uint32_t one, uint32_t neg1) {
         if constexpr (P < CF::V) {
             XY<CF> nxt = cur;
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst) nxt = load_xy<CF>(lamrow, s0 + P + 1);
             }
-            acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW, one, neg1);
+            acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW,
+                             !PBVD_SKIP_ROWS || s0 + P >= st_lo, one, neg1);
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst)
-                    Cycle<CF, P + 1, FULL>::run(pm, lamrow, flip, lg, drow, s0, nst, nxt, one, neg1);
+                    Cycle<CF, P + 1, FULL>::run(pm, lamrow, flip, lg, drow, s0, nst, st_lo, nxt, one,
+                                                neg1);
             }
         }
     }
@@ -430,7 +440,17 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     const bool edge = gw >= p.n_int_warps;
     const int e = int(gw - p.n_int_warps);
     if (edge && e >= p.n_edge) return;
+#ifdef PBVD_EXP_TIMING
+    auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+    if (p.dbg && lane == 0) {
+        unsigned smid; asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.dbg[4 * gw + 0] = gtime();
+        p.dbg[4 * gw + 3] = smid;
+    }
+#endif
     const int span = edge ? p.edges[e].span : p.span_int;
+    // first survivor row any traceback reads (tb.cuh: s_min = t0r + v)
+    const int s_read = min(span, (edge ? p.edges[e].t0r : p.t0r) + V);
     const int nchunks = (span + T - 1) / T;
     const int64_t wb0 = gw * BPW;              // launch-relative first interior block
 
@@ -651,12 +671,13 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         // survivor rows of this chunk, this lane's WPS words (direct stores:
         // each warp writes 32 * WPS contiguous words per stage)
         uint32_t* drow = gdec + size_t(c) * T * ROW + size_t(lane) * CF::WPS;
+        const int st_lo = s_read - c * T;     // rows below the traceback's first row: no store
         if (nst == T) {
 #pragma unroll 1
             for (int j = 0; j < CF::NCYC; ++j) {
                 const int s0 = j * V;
-                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, T, load_xy<CF>(lamrow, s0),
-                                        p.one, p.neg_one);
+                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, T, st_lo,
+                                        load_xy<CF>(lamrow, s0), p.one, p.neg_one);
                 transform(c + 1, j);     // harmless past the last chunk
             }
         } else {
@@ -664,10 +685,10 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             int s0 = 0;
 #pragma unroll 1
             for (; s0 + V <= nst; s0 += V)
-                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, nst, load_xy<CF>(lamrow, s0),
-                                        p.one, p.neg_one);
+                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, nst, st_lo,
+                                        load_xy<CF>(lamrow, s0), p.one, p.neg_one);
             if (s0 < nst)
-                Cycle<CF, 0, false>::run(pm, lamrow, flip, lg, drow, s0, nst,
+                Cycle<CF, 0, false>::run(pm, lamrow, flip, lg, drow, s0, nst, st_lo,
                                          load_xy<CF>(lamrow, s0), p.one, p.neg_one);
             if (next) {
 #pragma unroll 1
@@ -719,12 +740,19 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             ob[0] = p.edges[e].out_bit0;
         }
         const int nblk_tb = edge ? 1 : int(min(int64_t(BPW), int64_t(p.n_int) - wb0));
+#ifdef PBVD_EXP_TIMING
+        if (p.dbg && lane == 0) p.dbg[4 * gw + 1] = gtime();
+#endif
 #ifdef PBVD_EXP_NO_TB
         if (nblk_tb > 0) return;     // timing experiment only: skip the walk
 #endif
         warp_traceback<CF>(wbase, gdec, span, edge ? p.edges[e].t0r : p.t0r,
                            edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,
                            !edge && p.word_out, p.out, lane);
+#ifdef PBVD_EXP_TIMING
+        __syncwarp();
+        if (p.dbg && lane == 0) p.dbg[4 * gw + 2] = gtime();
+#endif
         return;
     }
     if (lg == 0) {

@@ -50,6 +50,7 @@ struct FwdParams {
     int64_t out_bit0;      // bit offset of the first interior block in out
     int t0r, t1r;          // interior decoding range relative to lo (L, L+D)
     int word_out;          // 1: interior blocks store aligned 32-bit words
+    unsigned long long* dbg;   // timing experiment only (PBVD_EXP_TIMING builds), else null
     EdgeDesc edges[MAX_EDGE];
 };
 

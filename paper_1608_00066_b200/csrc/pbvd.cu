@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -348,8 +349,32 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         const int fgrid = int((fp.n_int_warps + ne + v->NT / 32 - 1) / (v->NT / 32));
         const int ev = record(h, stream);
         if (ev >= 0) cudaEventRecord(h->ev_pool[ev], stream);
+#ifdef PBVD_EXP_TIMING
+        // timing experiment: per-warp (start, forward end, traceback end, smid)
+        static unsigned long long* dbg = nullptr;
+        const char* dump = std::getenv("PBVD_TIMING_DUMP");
+        const size_t ndbg = size_t(fgrid) * 4;
+        if (dump) {
+            if (dbg) cudaFree(dbg);
+            cudaMalloc(&dbg, ndbg * 8);
+            cudaMemsetAsync(dbg, 0, ndbg * 8, stream);
+            fp.dbg = dbg;
+        }
+#endif
         if (h->fused) v->fused(fgrid, stream, fp);
         else v->fwd(fgrid, stream, fp);
+#ifdef PBVD_EXP_TIMING
+        if (dump) {
+            std::vector<unsigned long long> hb(ndbg);
+            cudaMemcpyAsync(hb.data(), dbg, ndbg * 8, cudaMemcpyDeviceToHost, stream);
+            cudaStreamSynchronize(stream);
+            if (FILE* f = std::fopen(dump, "wb")) {
+                std::fwrite(hb.data(), 8, ndbg, f);
+                std::fclose(f);
+            }
+            fp.dbg = nullptr;
+        }
+#endif
         if (ev >= 0) {
             cudaEventRecord(h->ev_pool[ev + 1], stream);
             h->ev_fwd.push_back({ev, ev + 1});

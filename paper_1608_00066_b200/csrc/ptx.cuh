@@ -16,6 +16,14 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return d;
 }
 
+// (a & ~m) | (b & m) as one LOP3 (m an immediate mask): a bit-field insert
+template <uint32_t M>
+__device__ __forceinline__ uint32_t bit_insert(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(b), "r"(a), "n"(M));
+    return d;
+}
+
 // a - b + c as one IADD3; opaque to NVVM so it cannot re-associate the
 // decision computation across butterflies (which costs extra instructions).
 __device__ __forceinline__ uint32_t sub_add(uint32_t a, uint32_t b, uint32_t c) {
@@ -112,6 +120,10 @@ __device__ __forceinline__ void bulk_g2s_hint(uint32_t sdst, const void* gsrc, u
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
         "[%0], [%1], %2, [%3], %4;"
         ::"r"(sdst), "l"(gsrc), "r"(bytes), "r"(mbar), "l"(policy) : "memory");
+}
+// invalidate one 128-byte L2 line without writing it back (dead data)
+__device__ __forceinline__ void discard_l2_line(const void* g) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(g) : "memory");
 }
 // L2 prefetch of a global range (no completion tracking)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {

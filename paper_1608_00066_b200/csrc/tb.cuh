@@ -158,21 +158,37 @@ __device__ __forceinline__ uint32_t row_bit(RowT<CF> b, uint32_t q, uint32_t hbi
     if constexpr (CF::N == 64) return uint32_t(b >> q) & 1u;
     else return (b >> tb_bitpos<CF>(q, hbit)) & 1u;
 }
+// survivor bit of slot q moved to bit PH (other bits garbage): one variable
+// shift (+ one constant shift), so the dependent chain per step is
+// shift -> [shift] -> bit insert
 template <class CF, int PH>
-__device__ __forceinline__ void tbc_steps(TbState& t, const uint32_t* row, int woff, uint32_t sel,
-                                          uint32_t hbit) {
-    const RowT<CF> b = row_bits<CF>(row, woff, sel);
-    const uint32_t dec = row_bit<CF>(b, t.q, hbit);
-    t.acc64 = (t.acc64 << 1) | dec;
-    t.q = (t.q & ~(1u << PH)) | (dec << PH);
-    if constexpr (PH > 0) tbc_steps<CF, PH - 1>(t, row - CF::ROW, woff, sel, hbit);
+__device__ __forceinline__ uint32_t row_bit_at(RowT<CF> b, uint32_t q, uint32_t hbit) {
+    uint32_t x;
+    if constexpr (CF::N == 64) x = uint32_t(b >> q);
+    else x = b >> tb_bitpos<CF>(q, hbit);
+    return PH == 0 ? x : (x << PH);
+}
+template <class CF, int PH>
+__device__ __forceinline__ void tbc_steps(TbState& t, const RowT<CF> (&b)[CF::V], uint32_t hbit) {
+    const uint32_t xs = row_bit_at<CF, PH>(b[PH], t.q, hbit);
+    t.acc64 = (t.acc64 << 1) | ((xs >> PH) & 1u);
+    t.q = bit_insert<1u << PH>(t.q, xs);
+    if constexpr (PH > 0) tbc_steps<CF, PH - 1>(t, b, hbit);
+}
+template <class CF, int PH>
+__device__ __forceinline__ void tbc_load(RowT<CF> (&b)[CF::V], const uint32_t* row, int woff,
+                                         uint32_t sel) {
+    b[PH] = row_bits<CF>(row, woff, sel);
+    if constexpr (PH > 0) tbc_load<CF, PH - 1>(b, row - CF::ROW, woff, sel);
 }
 // v steps from row `row` (phase v-1) down, then the output word if complete
 template <class CF>
 __device__ __forceinline__ void tbc_cycle(TbState& t, const uint32_t* row, int woff, uint32_t sel,
                                           uint32_t hbit, uint32_t* out32, int64_t word0,
                                           int nwords) {
-    tbc_steps<CF, CF::V - 1>(t, row, woff, sel, hbit);
+    RowT<CF> b[CF::V];
+    tbc_load<CF, CF::V - 1>(b, row, woff, sel);
+    tbc_steps<CF, CF::V - 1>(t, b, hbit);
     const int eb = t.e, ea = t.e - CF::V;
     const int w = eb >> 5;
     if (eb >= 0 && (w << 5) > ea && w < nwords)
@@ -199,7 +215,8 @@ __device__ __forceinline__ void tbc_chunk(TbState& t, int lo, int hi, int c, Row
     constexpr int V = CF::V;
     if (hi - lo == TT && lo == c * TT) {
         const uint32_t* row = rows(hi - 1);
-#pragma unroll 1
+        // unrolled: the next cycle's row loads overlap this cycle's chain
+#pragma unroll
         for (int cy = 0; cy < TT / V; ++cy)
             tbc_cycle<CF>(t, row - cy * V * CF::ROW, woff, sel, hbit, out32, word0, nwords);
     } else {
@@ -430,19 +447,25 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
 // L2; while one warp walks (latency bound), the other warps of its SM
 // sub-partition keep the ALU pipes busy with their forward passes, and the
 // second launch and its grid-wide dependency disappear.
-template <class CF>
-struct TbwCfg {
-    static constexpr int NBUF = 3;
 #ifndef PBVD_TB_PREFETCH
 #define PBVD_TB_PREFETCH 0
 #endif
 #ifndef PBVD_FUSED_TT
 #define PBVD_FUSED_TT 18
 #endif
+#ifndef PBVD_TB_DISCARD
+#define PBVD_TB_DISCARD 0
+#endif
+#ifndef PBVD_FUSED_NBUF
+#define PBVD_FUSED_NBUF 3
+#endif
+template <class CF>
+struct TbwCfg {
+    static constexpr int NBUF = PBVD_FUSED_NBUF;             // ring depth (chunks)
     static constexpr int TT = CF::V * cmax(1, PBVD_FUSED_TT / CF::V);   // rows per chunk, multiple of v
     static constexpr int NBL = (CF::BPW + 31) / 32;         // blocks per lane
     static constexpr size_t RING = size_t(NBUF) * TT * CF::ROW * 4;
-    static constexpr size_t SMEM = RING + 64;
+    static constexpr size_t SMEM = RING + 8 * NBUF;
     static constexpr int WSH = TbCfg<CF>::WSH;
 };
 
@@ -589,6 +612,15 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
                 tbc_chunk<CF, TT>(t[m], lo, hi, c_top - k, [&](int r) { return slot_row(k, r); },
                                   woff[m], sel, hbit[m], out32, obit[m] >> 5, nwords);
             }
+#if PBVD_TB_DISCARD
+            // the chunk's survivor rows are dead now: drop their L2 lines
+            // without a write-back (they were read into the ring already)
+            {
+                const uint8_t* g0 = reinterpret_cast<const uint8_t*>(region + size_t(lo) * ROW);
+                const int nl = (hi - lo) * ROW * 4 / 128;
+                for (int i = lane; i < nl; i += 32) discard_l2_line(g0 + size_t(i) * 128);
+            }
+#endif
             __syncwarp();          // slot k % NBUF free for chunk k + NBUF
         }
         return;

@@ -33,8 +33,19 @@ def supported():
     return out
 
 
+def probe_acs_balanced(device: int = 0):
+    """pbvd_probe_acs_balanced: (measured ACS/s of the pipe-balanced minimal
+    sequence, kernel ms)."""
+    L = _lib.load()
+    a, m = ctypes.c_double(), ctypes.c_double()
+    _check(L.pbvd_probe_acs_balanced(int(device), ctypes.byref(a), ctypes.byref(m)), None,
+           "pbvd_probe_acs_balanced")
+    return a.value, m.value
+
+
 def probe_acs_peak(device: int = 0):
-    """pbvd_probe_acs_peak: (measured ACS/s roofline, kernel ms)."""
+    """pbvd_probe_acs_peak: (measured ACS/s of the all-ALU minimal sequence,
+    kernel ms)."""
     L = _lib.load()
     a, m = ctypes.c_double(), ctypes.c_double()
     _check(L.pbvd_probe_acs_peak(int(device), ctypes.byref(a), ctypes.byref(m)), None,

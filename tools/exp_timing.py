@@ -1,0 +1,38 @@
+"""Per-warp timeline of one fused decode (PBVD_EXP_TIMING build): start,
+forward end, traceback end per warp (globaltimer ns), summarised."""
+import os
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+import torch
+import synth
+import paper_1608_00066_b200 as P
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else synth.CONFIGS[cfg]["n_info"]
+c = synth.CONFIGS[cfg]
+code, punct = synth.CODES[c["code"]], synth.PUNCT[c["punct"]]
+info, llr = synth.make_stream(code, n, c["ebn0"], c["seed"], punct, c["hard"], device="cuda")
+dec = P.Decoder(code["K"], code["polys"], c["D"], c["L"], punct=punct)
+dec.decode(llr, n)
+torch.cuda.synchronize()
+os.environ["PBVD_TIMING_DUMP"] = "/tmp/pbvd_timing.bin"
+dec.decode(llr, n)
+torch.cuda.synchronize()
+a = np.fromfile("/tmp/pbvd_timing.bin", dtype=np.uint64).reshape(-1, 4).astype(np.int64)
+a = a[a[:, 0] > 0]
+t0 = a[:, 0].min()
+st, fe, te, sm = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3, a[:, 3]
+print(f"{cfg} n={n} warps={len(a)}  kernel span {te.max():.1f} us")
+print(f"start: min {st.min():.1f} max {st.max():.1f} us")
+print(f"fwd end: min {fe.min():.1f} p10 {np.percentile(fe,10):.1f} p50 {np.percentile(fe,50):.1f} p90 {np.percentile(fe,90):.1f} max {fe.max():.1f}")
+tb = te - fe
+print(f"tb dur: min {tb.min():.1f} p10 {np.percentile(tb,10):.1f} p50 {np.percentile(tb,50):.1f} p90 {np.percentile(tb,90):.1f} max {tb.max():.1f}")
+fw = fe - st
+print(f"fwd dur: min {fw.min():.1f} p50 {np.percentile(fw,50):.1f} max {fw.max():.1f}")
+# per-SM warp counts vs forward duration
+cnt = np.bincount(sm, minlength=148)
+print("warps per SM histogram:", np.bincount(cnt))
+for k in sorted(set(cnt[sm])):
+    sel = cnt[sm] == k
+    print(f"  SMs with {k} warps: fwd dur p50 {np.percentile(fw[sel],50):.1f} max {fw[sel].max():.1f}; tb p50 {np.percentile(tb[sel],50):.1f}")
