@@ -444,8 +444,8 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
     if (p.dbg && lane == 0) {
         unsigned smid; asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        p.dbg[4 * gw + 0] = gtime();
-        p.dbg[4 * gw + 3] = smid;
+        p.dbg[8 * gw + 0] = gtime();
+        p.dbg[8 * gw + 3] = smid;
     }
 #endif
     const int span = edge ? p.edges[e].span : p.span_int;
@@ -741,17 +741,24 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         }
         const int nblk_tb = edge ? 1 : int(min(int64_t(BPW), int64_t(p.n_int) - wb0));
 #ifdef PBVD_EXP_TIMING
-        if (p.dbg && lane == 0) p.dbg[4 * gw + 1] = gtime();
+        if (p.dbg && lane == 0) p.dbg[8 * gw + 1] = gtime();
 #endif
 #ifdef PBVD_EXP_NO_TB
         if (nblk_tb > 0) return;     // timing experiment only: skip the walk
 #endif
         warp_traceback<CF>(wbase, gdec, span, edge ? p.edges[e].t0r : p.t0r,
                            edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,
-                           !edge && p.word_out, p.out, lane);
+                           p.word_out && (!edge || (((ob[0] | int64_t(p.edges[e].t1r -
+                                                                        p.edges[e].t0r)) & 31) == 0)),
+                           p.out, lane,
+#ifdef PBVD_EXP_TIMING
+                           p.dbg ? p.dbg + 8 * gw : nullptr);
+#else
+                           nullptr);
+#endif
 #ifdef PBVD_EXP_TIMING
         __syncwarp();
-        if (p.dbg && lane == 0) p.dbg[4 * gw + 2] = gtime();
+        if (p.dbg && lane == 0) p.dbg[8 * gw + 2] = gtime();
 #endif
         return;
     }

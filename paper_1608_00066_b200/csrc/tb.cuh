@@ -343,9 +343,10 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
     const uint32_t hbit = 16u * uint32_t(h);
     const int woff = g * W * WPS;
     const int nbits = t1r - t0r;
-    // words: interior blocks store aligned 32-bit words; edge blocks stage
-    // their (possibly partial) words through a local buffer and store bytes
-    const bool words = (!edge) && p.word_out;
+    // words: blocks whose bits start on a 32-bit word and fill whole words
+    // store aligned words; others (partial last block, unaligned output) bytes
+    // (edge blocks too when their bits start on a word and fill whole words)
+    const bool words = p.word_out && (!edge || (((out_bit0 | int64_t(t1r - t0r)) & 31) == 0));
     uint32_t* out32 = reinterpret_cast<uint32_t*>(p.out);
     const int64_t word0 = out_bit0 >> 5;
     const int nwords = (nbits + 31) >> 5;
@@ -474,7 +475,8 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
                                                int t0r, int t1r, int nblk,
                                                const uint32_t (&st)[TbwCfg<CF>::NBL],
                                                const int64_t (&obit)[TbwCfg<CF>::NBL], bool words,
-                                               uint8_t* out, int lane) {
+                                               uint8_t* out, int lane,
+                                               unsigned long long* dbg = nullptr) {
     using TC = TbwCfg<CF>;
     constexpr int V = CF::V, W = CF::W, WPS = CF::WPS, ROW = CF::ROW;
     constexpr int TT = TC::TT, NBUF = TC::NBUF, NBL = TC::NBL;
@@ -600,9 +602,19 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
     }
 
     if constexpr (tb_compact<CF>()) {
+#ifdef PBVD_EXP_TIMING
+        long long cw = 0, cc = 0;
+#endif
         for (int k = 0; k < nchunks; ++k) {
+#ifdef PBVD_EXP_TIMING
+            const long long c0 = clock64();
+#endif
             if (k + NBUF - 1 < nchunks) issue(k + NBUF - 1);
             wait(k);
+#ifdef PBVD_EXP_TIMING
+            const long long c1 = clock64();
+            cw += c1 - c0;
+#endif
             int lo, hi;
             chunk_rows(k, lo, hi);
 #pragma unroll
@@ -612,6 +624,10 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
                 tbc_chunk<CF, TT>(t[m], lo, hi, c_top - k, [&](int r) { return slot_row(k, r); },
                                   woff[m], sel, hbit[m], out32, obit[m] >> 5, nwords);
             }
+#ifdef PBVD_EXP_TIMING
+            cc += clock64() - c1;
+            if (dbg && lane == 0 && k == nchunks - 1) { dbg[4] = cw; dbg[5] = cc; dbg[6] = nchunks; }
+#endif
 #if PBVD_TB_DISCARD
             // the chunk's survivor rows are dead now: drop their L2 lines
             // without a write-back (they were read into the ring already)

@@ -19,7 +19,7 @@ torch.cuda.synchronize()
 os.environ["PBVD_TIMING_DUMP"] = "/tmp/pbvd_timing.bin"
 dec.decode(llr, n)
 torch.cuda.synchronize()
-a = np.fromfile("/tmp/pbvd_timing.bin", dtype=np.uint64).reshape(-1, 4).astype(np.int64)
+a = np.fromfile("/tmp/pbvd_timing.bin", dtype=np.uint64).reshape(-1, 8).astype(np.int64)
 a = a[a[:, 0] > 0]
 t0 = a[:, 0].min()
 st, fe, te, sm = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3, a[:, 3]
@@ -30,6 +30,15 @@ tb = te - fe
 print(f"tb dur: min {tb.min():.1f} p10 {np.percentile(tb,10):.1f} p50 {np.percentile(tb,50):.1f} p90 {np.percentile(tb,90):.1f} max {tb.max():.1f}")
 fw = fe - st
 print(f"fwd dur: min {fw.min():.1f} p50 {np.percentile(fw,50):.1f} max {fw.max():.1f}")
+wc, cc, nch = a[:, 4], a[:, 5], a[:, 6]
+ok = nch > 0
+print(f"tb wait cycles/chunk: p50 {np.percentile(wc[ok]/nch[ok],50):.0f} p90 {np.percentile(wc[ok]/nch[ok],90):.0f}; "
+      f"walk cycles/chunk: p50 {np.percentile(cc[ok]/nch[ok],50):.0f} p90 {np.percentile(cc[ok]/nch[ok],90):.0f}; chunks {np.median(nch[ok]):.0f}")
+late = te > np.percentile(te, 75)
+print(f"late warps: wait/chunk p50 {np.percentile((wc/np.maximum(nch,1))[late & ok],50):.0f} walk/chunk p50 {np.percentile((cc/np.maximum(nch,1))[late & ok],50):.0f}")
+idx = np.argsort(te)[-6:]
+for i in idx:
+    print(f"  warp {i}: sm {sm[i]} start {st[i]:.1f} fwd_end {fe[i]:.1f} tb {tb[i]:.1f} us; wait/ch {wc[i]/max(nch[i],1):.0f} walk/ch {cc[i]/max(nch[i],1):.0f} cyc")
 # per-SM warp counts vs forward duration
 cnt = np.bincount(sm, minlength=148)
 print("warps per SM histogram:", np.bincount(cnt))
