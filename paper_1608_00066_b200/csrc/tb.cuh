@@ -166,7 +166,15 @@ __device__ __forceinline__ uint32_t row_bit_at(RowT<CF> b, uint32_t q, uint32_t 
     uint32_t x;
     if constexpr (CF::N == 64) x = uint32_t(b >> q);
     else x = b >> tb_bitpos<CF>(q, hbit);
-    return PH == 0 ? x : (x << PH);
+    if constexpr (PH == 0) {
+        return x;
+    } else {
+        // funnel shift (ALU pipe, like the shift before and the insert after:
+        // no cross-pipe latency on the walk's dependent chain)
+        uint32_t y;
+        asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(y) : "r"(x), "n"(PH));
+        return y;
+    }
 }
 template <class CF, int PH>
 __device__ __forceinline__ void tbc_steps(TbState& t, const RowT<CF> (&b)[CF::V], uint32_t hbit) {
