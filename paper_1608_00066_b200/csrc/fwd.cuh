@@ -51,6 +51,9 @@
 #include "tb.cuh"
 
 // compile-time experiment switches (defaults are the measured best)
+#ifndef PBVD_DIRECT_SOFT
+#define PBVD_DIRECT_SOFT 0
+#endif
 #ifndef PBVD_SKIP_ROWS
 #define PBVD_SKIP_ROWS 0
 #endif
@@ -132,7 +135,11 @@ struct Cfg {
     static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
-    static constexpr size_t WLAM = size_t(2) * PPW * LSTR * 4;     // double buffered
+    // R = 2: the ACS loop reads each stage's two soft bytes of both blocks
+    // straight from the (2-byte aligned) raw / depunctured windows -- no
+    // transform pass and no operand buffer
+    static constexpr bool DIRECT = (R == 2) && PBVD_DIRECT_SOFT;
+    static constexpr size_t WLAM = DIRECT ? 0 : size_t(2) * PPW * LSTR * 4;   // double buffered
     static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
     static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
@@ -186,6 +193,28 @@ __device__ __forceinline__ XY<CF> load_xy(const uint32_t* lamrow, int s) {
     }
     return r;
 }
+
+// Soft-value source of the ACS loop: the transformed per-pair words (lam
+// row), or -- DIRECT, R = 2 -- the two blocks' windows read in place: one
+// 16-bit load per block, interleaved [uA0, uB0, uA1, uB1] and biased by PRMT
+// and one XOR.
+template <class CF>
+struct SoftSrc {
+    const uint32_t* lamrow = nullptr;
+    const uint8_t* a = nullptr;          // stage 0 of the chunk, block A window
+    const uint8_t* b = nullptr;          // same, block B
+    __device__ __forceinline__ XY<CF> load(int s) const {
+        if constexpr (CF::DIRECT) {
+            XY<CF> r;
+            const uint32_t x = *reinterpret_cast<const uint16_t*>(a + 2 * s);
+            const uint32_t y = *reinterpret_cast<const uint16_t*>(b + 2 * s);
+            r.v[0] = prmt(x, y, 0x5140u) ^ 0x80808080u;
+            return r;
+        } else {
+            return load_xy<CF>(lamrow, s);
+        }
+    }
+};
 
 // The 2^R codeword metrics of one stage for a block pair, permuted by the
 // lane's alpha offset: Pv[c] = BM'(c ^ flip) with the biased metric
@@ -390,20 +419,20 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
 // metrics with stage P's butterflies).
 template <class CF, int P, bool FULL>
 struct Cycle {
-    static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const uint32_t* lamrow,
+    static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const SoftSrc<CF>& src,
                                                const int (&flip)[CF::V], int lg, uint32_t* drow,
                                                int s0, int nst, int st_lo, const XY<CF>& cur,
                                                uint32_t one, uint32_t neg1) {
         if constexpr (P < CF::V) {
             XY<CF> nxt = cur;
             if constexpr (P + 1 < CF::V) {
-                if (FULL || s0 + P + 1 < nst) nxt = load_xy<CF>(lamrow, s0 + P + 1);
+                if (FULL || s0 + P + 1 < nst) nxt = src.load(s0 + P + 1);
             }
             acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW,
                              !PBVD_SKIP_ROWS || s0 + P >= st_lo, one, neg1);
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst)
-                    Cycle<CF, P + 1, FULL>::run(pm, lamrow, flip, lg, drow, s0, nst, st_lo, nxt, one,
+                    Cycle<CF, P + 1, FULL>::run(pm, src, flip, lg, drow, s0, nst, st_lo, nxt, one,
                                                 neg1);
             }
         }
@@ -640,34 +669,56 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         gdec = p.dec_edge + size_t(e) * size_t(p.span_edge_max) * ROW;
     }
 
-    issue_raw(0);
-    if (nchunks > 1) issue_raw(1);
-    if (nchunks > 1) cp_async_wait<1>(); else cp_async_wait<0>();
-    __syncwarp();
-    if (p.P != 1) {
-        depuncture(0);
+    if constexpr (CF::DIRECT) {
+        issue_raw(0);
+    } else {
+        issue_raw(0);
+        if (nchunks > 1) issue_raw(1);
+        if (nchunks > 1) cp_async_wait<1>(); else cp_async_wait<0>();
+        __syncwarp();
+        if (p.P != 1) {
+            depuncture(0);
+            __syncwarp();
+        }
+#pragma unroll 1
+        for (int j = 0; j < CF::NCYC; ++j) transform(0, j);
         __syncwarp();
     }
-#pragma unroll 1
-    for (int j = 0; j < CF::NCYC; ++j) transform(0, j);
-    __syncwarp();
     for (int c = 0; c < nchunks; ++c) {
         const int nst = min(T, span - c * T);
         const bool next = c + 1 < nchunks;
-        // soft windows of chunk c+2 go in flight; those of chunk c+1 (issued a
-        // chunk ago) must have landed before this chunk's transform slices
-        if (c + 2 < nchunks) {
-            issue_raw(c + 2);
-            cp_async_wait<1>();
-        } else {
+        SoftSrc<CF> src;
+        if constexpr (CF::DIRECT) {
+            // chunk c's windows (issued a chunk ago) land; chunk c+1's go in
+            // flight into the other buffer (chunk c-1, its reader, is done)
             cp_async_wait<0>();
-        }
-        __syncwarp();
-        if (next && p.P != 1) {
-            depuncture(c + 1);
             __syncwarp();
+            if (next) issue_raw(c + 1);
+            const bool dense = (p.P == 1);
+            if (!dense) {
+                depuncture(c);
+                __syncwarp();
+            }
+            const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
+            const int iA = edge ? 0 : 2 * grp, iB = edge ? 0 : 2 * grp + 1;
+            src.a = rb + size_t(iA) * RAWB + (dense ? woffs[(c & 1) * BPW + iA] : 0);
+            src.b = rb + size_t(iB) * RAWB + (dense ? woffs[(c & 1) * BPW + iB] : 0);
+        } else {
+            // soft windows of chunk c+2 go in flight; those of chunk c+1 (issued a
+            // chunk ago) must have landed before this chunk's transform slices
+            if (c + 2 < nchunks) {
+                issue_raw(c + 2);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncwarp();
+            if (next && p.P != 1) {
+                depuncture(c + 1);
+                __syncwarp();
+            }
+            src.lamrow = lam + size_t(c & 1) * PPW * LSTR + size_t(edge ? 0 : grp) * LSTR;
         }
-        const uint32_t* lamrow = lam + size_t(c & 1) * PPW * LSTR + size_t(edge ? 0 : grp) * LSTR;
         // survivor rows of this chunk, this lane's WPS words (direct stores:
         // each warp writes 32 * WPS contiguous words per stage)
         uint32_t* drow = gdec + size_t(c) * T * ROW + size_t(lane) * CF::WPS;
@@ -676,23 +727,25 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
 #pragma unroll 1
             for (int j = 0; j < CF::NCYC; ++j) {
                 const int s0 = j * V;
-                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, T, st_lo,
-                                        load_xy<CF>(lamrow, s0), p.one, p.neg_one);
-                transform(c + 1, j);     // harmless past the last chunk
+                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, T, st_lo, src.load(s0),
+                                        p.one, p.neg_one);
+                if constexpr (!CF::DIRECT) transform(c + 1, j);     // harmless past the last chunk
             }
         } else {
             // partial (last) chunk: whole cycles unguarded, then the remainder
             int s0 = 0;
 #pragma unroll 1
             for (; s0 + V <= nst; s0 += V)
-                Cycle<CF, 0, true>::run(pm, lamrow, flip, lg, drow, s0, nst, st_lo,
-                                        load_xy<CF>(lamrow, s0), p.one, p.neg_one);
+                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, nst, st_lo, src.load(s0),
+                                        p.one, p.neg_one);
             if (s0 < nst)
-                Cycle<CF, 0, false>::run(pm, lamrow, flip, lg, drow, s0, nst, st_lo,
-                                         load_xy<CF>(lamrow, s0), p.one, p.neg_one);
-            if (next) {
+                Cycle<CF, 0, false>::run(pm, src, flip, lg, drow, s0, nst, st_lo, src.load(s0),
+                                         p.one, p.neg_one);
+            if constexpr (!CF::DIRECT) {
+                if (next) {
 #pragma unroll 1
-                for (int j = 0; j < CF::NCYC; ++j) transform(c + 1, j);
+                    for (int j = 0; j < CF::NCYC; ++j) transform(c + 1, j);
+                }
             }
         }
         // renormalise: subtract the block minimum (per 16-bit half = per block)

@@ -42,6 +42,8 @@ using namespace pbvd;
 struct Workspace {
     void* p = nullptr;
     size_t bytes = 0;
+    void* al = nullptr;       // realigned soft window (odd caller pointers only)
+    size_t al_bytes = 0;
 };
 
 // Resources of the host-buffer pipeline (pbvd_decode_host): per stream a
@@ -177,6 +179,16 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     }
     int rc = ensure_prepared(h, v);
     if (rc) return rc;
+    if (v->direct && h->P == 1 && (reinterpret_cast<uintptr_t>(llr) & 1)) {
+        // the forward kernel reads each stage's two soft bytes with one
+        // 16-bit load: an odd caller pointer is realigned through a copy
+        const size_t nb2 = size_t(n_llr_win);
+        rc = ensure_buf(h, &W.al, &W.al_bytes, nb2);
+        if (rc) return rc;
+        cudaError_t e = cudaMemcpyAsync(W.al, llr, nb2, cudaMemcpyDeviceToDevice, stream);
+        if (e != cudaSuccess) return cuda_fail(h, e, "realign copy");
+        llr = static_cast<const int8_t*>(W.al);
+    }
 
     // interior blocks: lo = bD - L >= 0, b < nb-1, (b+1)D + L <= n_stages
     const int64_t D = h->D, L = h->L;
@@ -469,8 +481,10 @@ void pbvd_destroy(pbvd_t h) {
     {
         DeviceGuard g(h->device);
         if (h->ws.p) cudaFree(h->ws.p);
+        if (h->ws.al) cudaFree(h->ws.al);
         for (auto& ln : h->lanes) {
             if (ln.ws.p) cudaFree(ln.ws.p);
+            if (ln.ws.al) cudaFree(ln.ws.al);
             if (ln.d_llr) cudaFree(ln.d_llr);
             if (ln.d_bits) cudaFree(ln.d_bits);
             if (ln.stream) cudaStreamDestroy(ln.stream);

@@ -17,6 +17,7 @@ struct Variant {
     int K, R, W;
     uint32_t polys[4];
     int BPC, BPW, NT, T, ROW, NR_TB, TT, BOXB;
+    bool direct;        // reads R = 2 soft bytes with 16-bit loads: needs an even llr address
     size_t smem_fwd, smem_tb, smem_fused;
     int default_rank;   // lower = preferred default for the code
     cudaError_t (*prepare)();

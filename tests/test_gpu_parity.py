@@ -144,3 +144,28 @@ def test_compute_sanitizer_memcheck_clean(pbvd):
                            capture_output=True, text=True, timeout=600, cwd=root)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         assert "bad bytes: 0" in r.stdout
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_odd_aligned_soft_pointer(pbvd, orc, fused):
+    """The R = 2 forward kernel reads a stage's two soft bytes with one 16-bit
+    load; a caller buffer at an odd address is realigned by the library and
+    decodes bit-exactly (whole stream and a block-range window)."""
+    code = synth.CODES["k7"]
+    n_info, D, L = 20000, 512, 42
+    info, llr = synth.make_stream(code, n_info, 3.0, 77)
+    want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, D, L))
+    buf = torch.empty(llr.numel() + 1, dtype=torch.int8, device="cuda")
+    buf[1:].copy_(llr.cuda())
+    odd = buf[1:]
+    assert odd.data_ptr() % 2 == 1
+    dec = pbvd.Decoder(code["K"], code["polys"], D, L, fused=fused)
+    got = dec.decode(odd, n_info).cpu().numpy()
+    assert (got == want).all()
+    # a block range from an odd window start (stage 2*D - L)
+    b0, nb = 2, 10
+    lo = b0 * D - L
+    hi = (b0 + nb) * D + L
+    win = buf[1 + 2 * lo: 1 + 2 * hi]
+    part = dec.decode_blocks(win, lo, n_info, b0, nb).cpu().numpy()
+    assert (part == want[b0 * D // 8:(b0 + nb) * D // 8]).all()
