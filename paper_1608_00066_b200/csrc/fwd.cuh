@@ -51,6 +51,9 @@
 #include "tb.cuh"
 
 // compile-time experiment switches (defaults are the measured best)
+#ifndef PBVD_DSCHEME
+#define PBVD_DSCHEME 1
+#endif
 #ifndef PBVD_DIRECT_SOFT
 #define PBVD_DIRECT_SOFT 0
 #endif
@@ -358,6 +361,34 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
 #pragma unroll
         for (int c = 0; c < NC; ++c) PC[c] = add32(Pv[c], 0x7FFF7FFFu);
         constexpr int pb = 1 << P;
+        if constexpr (PBVD_DSCHEME && NC <= 4) {
+        // d-scheme: t = (E - O) + (PC_own - BM_other), the same 32-bit sum as
+        // E - m_other + PC_own, with E - O shared by the butterfly's two
+        // outputs and every add two-operand (either pipe): 3.5 instructions
+        // per output like the IADD3/IMAD split, but free to balance the ALU and
+        // FMA pipes (R = 2; for R = 3 the 8 extra per-stage constants cost
+        // more than they save)
+        uint32_t KC[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) KC[c] = PC[c] - Pv[c ^ g0];
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            if (k & pb) continue;
+            const int a = CF::alpha_reg(k, P);
+            const uint32_t E = pm[k], O = pm[k | pb];
+            const uint32_t mO0 = add32(O, Pv[a ^ g0]);
+            const uint32_t nE = __viaddmin_s16x2(E, Pv[a], mO0);
+            const uint32_t mO1 = add32(O, Pv[a ^ gK ^ g0]);
+            const uint32_t nO = __viaddmin_s16x2(E, Pv[a ^ gK], mO1);
+            const uint32_t d = imad(O, neg1, E);
+            pm[k] = nE;
+            pm[k | pb] = nO;
+            t[k] = add32(d, KC[a]);
+            t[k | pb] = add32(d, KC[a ^ gK]);
+        }
+        pack_store<CF>(t, 0u, drow, st);
+        return;
+        }
 #pragma unroll
         for (int k = 0; k < S; ++k) {
             if (k & pb) continue;
