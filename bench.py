@@ -136,22 +136,24 @@ class ClockSampler:
 
 # ---- ACS roofline derived from unit counts and clocks ----
 # Minimal instruction sequence per warp-level packed output (one 16x2 register
-# = one state of two blocks, x 32 lanes = 64 ACS):
-#   VIADDMNMX.S16x2 (ALU)  + other-candidate add (FMA as IMAD.IADD)
-#   + decision operand: IADD3 (ALU) or 2 x IMAD (FMA), fraction f on FMA
-#   + 15/16 packing instr (PRMT 1/2 + LOP3 7/16, ALU)
+# = one state of two blocks, x 32 lanes = 64 ACS), the kernel's d-scheme:
+#   VIADDMNMX.S16x2 (ALU) + 15/16 packing instr (PRMT 1/2 + LOP3 7/16, ALU)
+#   + other-candidate add + decision add + half of the shared E - O
+#     (2.5 two-operand adds, each on the ALU or the FMA pipe)
 # Pipe model (B300_MICROARCH.md "Pipe rates"): ALU and FMA reciprocal
 # throughput 2 cycles per SM sub-partition each, issue 1 instr/cycle.
-PACK_ALU = 0.5 + 7.0 / 16.0
+ALU_ONLY = 1.0 + 0.5 + 7.0 / 16.0
+FLEX = 2.5
 
 
 def acs_sol_cycles():
-    """min over f of max(issue, ALU, FMA) cycles per packed output."""
+    """min over the ALU/FMA split of max(issue, 2*ALU, 2*FMA) cycles per
+    packed output; returns (cycles, fraction of the flexible adds on FMA)."""
     best = None
     for i in range(0, 1001):
         f = i / 1000.0
-        alu = 1.0 + PACK_ALU + (1.0 - f)
-        fma = 1.0 + 2.0 * f
+        alu = ALU_ONLY + FLEX * (1.0 - f)
+        fma = FLEX * f
         c = max(alu + fma, 2.0 * alu, 2.0 * fma)
         if best is None or c < best[0]:
             best = (c, f)
@@ -403,7 +405,7 @@ def run_ours(args):
                         f"{sm_mhz:.0f} MHz (median SM clock under load) x 64 ACS per "
                         f"{sol_cycles:.3f} cycles (minimal 16x2 ACS+decision sequence, "
                         f"ALU/FMA pipes at 0.5 and issue at 1 instr/cycle, "
-                        f"{sol_f:.2f} of decision operands on FMA)"),
+                        f"{sol_f:.2f} of the two-operand adds on FMA)"),
         "probe_all_alu_tacs": probe_acs / 1e12,
         "probe_balanced_tacs": probe_bal / 1e12,
         "acs_per_launch": acs_step, "kernel_ms": fwd_ms, "tb_kernel_ms": tb_ms,
