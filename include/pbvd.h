@@ -148,8 +148,10 @@ int pbvd_get_lanes(pbvd_t h);
 int pbvd_set_fused(pbvd_t h, int fused);
 int pbvd_get_fused(pbvd_t h);
 
-/* Upper bound on the survivor workspace in bytes (default 4 GiB); decodes
- * larger than one workspace run in waves. */
+/* Upper bound on the survivor workspace in bytes (default 4 GiB: measured
+ * best for C5 on B200 -- larger waves lose to address-translation misses);
+ * decodes larger than one workspace run in waves.  Returns PBVD_EINVAL below
+ * 1 MiB. */
 int pbvd_set_workspace_limit(pbvd_t h, size_t bytes);
 
 /* When enabled, each decode records CUDA events around every kernel launch

@@ -277,8 +277,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
                   (((I0 - B0) * D) % 32 == 0);
 
     // ---- launch groups: interior waves; head edges ride with the first wave,
-    // tail edges with the last, unless a group's soft window would exceed the
-    // TMA coordinate range (then edges get their own launches)
+    // tail edges with the last (at most MAX_EDGE per launch; the kernel
+    // addresses the soft window with 64-bit offsets, so a wave may be any size)
     struct Group {
         int64_t i0, i1;                 // interior blocks [i0, i1)
         std::vector<EdgeDesc> edges;
@@ -308,18 +308,14 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         klo = kept_before_h(h, slo);
         khi = kept_before_h(h, shi);
     };
-    const int64_t kLimit = (int64_t(1) << 31) - 4096;
-    {   // split oversized groups / too many edges
+    {   // too many edges for one launch: the rest get their own launches
         std::vector<Group> out;
         for (auto& g : groups) {
-            int64_t klo, khi;
-            group_range(g, klo, khi);
-            const bool big = (khi - klo) > kLimit;
             Group core{g.i0, g.i1, {}, {}};
             std::vector<Group> extra;
             for (size_t k = 0; k < g.edges.size(); ++k) {
                 Group* tgt = nullptr;
-                if (!big && core.edges.size() < size_t(MAX_EDGE)) tgt = &core;
+                if (core.edges.size() < size_t(MAX_EDGE)) tgt = &core;
                 if (!tgt) {
                     if (extra.empty() || extra.back().edges.size() >= size_t(MAX_EDGE))
                         extra.push_back({0, 0, {}, {}});
@@ -339,8 +335,6 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         const int ne = int(g.edges.size());
         int64_t klo, khi;
         group_range(g, klo, khi);
-        if (khi - klo > kLimit + 4096)
-            return fail(h, PBVD_EUNSUPPORTED, "a single block's soft window exceeds 2 GiB");
         fp.llr = llr + (klo - kb_ws0);
         fp.kb_ws0 = klo;
         fp.n_llr = khi - klo;

@@ -127,3 +127,23 @@ def test_host_pipeline_matches_device_path(P):
         dev = dec.decode(llr.cuda(), n_info).cpu()
         host = dec.decode_host(llr.pin_memory(), n_info, n_streams=3)
         assert torch.equal(host, dev)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_many_waves_equal_one_wave(P, fused):
+    """A small survivor-workspace limit splits the decode into many waves
+    (interior-block groups, edges riding with the first / last); the bits are
+    identical to a one-wave decode."""
+    code = synth.CODES["k7"]
+    n_info = 1 << 22
+    info, llr = synth.make_stream(code, n_info, 3.0, 31, device="cuda")
+    ref = P.Decoder(code["K"], code["polys"], 512, 42, fused=fused)
+    want = ref.decode(llr, n_info).cpu()
+    dec = P.Decoder(code["K"], code["polys"], 512, 42, fused=fused)
+    dec.set_workspace_limit(8 << 20)
+    dec.set_profiling(True)
+    got = dec.decode(llr, n_info).cpu()
+    torch.cuda.synchronize()
+    _, _, launches = dec.kernel_times()
+    assert launches >= 8
+    assert torch.equal(got, want)
