@@ -62,16 +62,21 @@ enum pbvd_status {
     PBVD_EINVAL = -1,       /* bad argument (null pointer, range)              */
     PBVD_ENOMEM = -2,       /* device or host allocation failed                */
     PBVD_ECUDA = -3,        /* CUDA runtime / launch error                     */
-    PBVD_EUNSUPPORTED = -4, /* code has no compiled kernel (see pbvd_supported) */
+    PBVD_EUNSUPPORTED = -4, /* no compiled kernel and the run-time (NVRTC) build
+                               failed or the lane count is not a supported shape */
     PBVD_ESIZE = -5         /* buffer length inconsistent with n_info          */
 };
 
 #define PBVD_TERMINATED (1u << 0) /* stream ends with K-1 zero tail stages (c-13) */
+#define PBVD_ALLOW_CATASTROPHIC (1u << 1) /* accept generators with no g_{K-1} or no g_0
+                                            tap (SPEC S:53-55 warning-class override) */
 
 /* Create a decoder on CUDA device `device`.
- *   K          constraint length (3..9 compiled)
+ *   K          constraint length, 3..9
  *   R          generators per code (code rate 1/R before puncturing), 2..4
- *   polys      R generator polynomials (see Conventions); host pointer
+ *   polys      R generator polynomials (see Conventions); host pointer; each
+ *              in [1, 2^K); some polynomial must have bit K-1 and some bit 0
+ *              set unless flags has PBVD_ALLOW_CATASTROPHIC
  *   punct_period P >= 1; 1 = unpunctured
  *   punct      R*P keep flags, row r (generator r) then column p, i.e.
  *              punct[r*P + p]; host pointer, NULL iff P == 1.  Column p
@@ -80,9 +85,15 @@ enum pbvd_status {
  *              whole output bytes)
  *   L          truncation / traceback length (M = L), 1 <= L
  *   soft_bits  quantisation of the input, 1..8 (1 = hard +-1); advisory only
- *   flags      PBVD_TERMINATED or 0
- * Returns PBVD_EUNSUPPORTED if no kernel is compiled for (K, R, polys);
- * pbvd_supported() lists them. */
+ *   flags      PBVD_TERMINATED | PBVD_ALLOW_CATASTROPHIC, or 0
+ * Kernels: the codes listed by pbvd_supported() are compiled into the
+ * library; any other (K, R, polys) is compiled at create time from the same
+ * kernel templates with NVRTC (libnvrtc.so.12 loaded on demand; a few seconds
+ * the first time, then cached in-process and on disk under $PBVD_JIT_CACHE,
+ * default ~/.cache/pbvd_jit; PBVD_JIT_CACHE=off disables the disk cache).
+ * Returns PBVD_EINVAL for bad arguments, PBVD_ECUDA for a bad device and
+ * PBVD_EUNSUPPORTED if the run-time build fails; pbvd_last_error(NULL) then
+ * gives the reason (thread-local). */
 int pbvd_create(pbvd_t *out, int K, int R, const uint32_t *polys, int punct_period,
                 const uint8_t *punct, int D, int L, int soft_bits, unsigned flags,
                 int device);
@@ -167,6 +178,7 @@ typedef struct {
     int64_t dec_bytes_per_block; /* survivor bytes of one interior block   */
     int64_t span;                /* forward stages of one interior block   */
     size_t workspace_bytes;      /* currently allocated                    */
+    int jit;                     /* 1 if the kernels were built at run time */
 } pbvd_info;
 int pbvd_get_info(pbvd_t h, pbvd_info *info);
 
@@ -183,10 +195,22 @@ int pbvd_probe_acs_peak(int device, double *acs_per_s, double *ms);
  * roofline bench.py reports.  Same arguments/errors. */
 int pbvd_probe_acs_balanced(int device, double *acs_per_s, double *ms);
 
-/* Compiled (K, R, polys...) combinations, as text "K:R:o1,o2[,o3]:lanes;..." */
+/* Compiled (K, R, polys...) combinations, as text "K:R:o1,o2[,o3]:lanes;..."
+ * (other codes are built at run time, see pbvd_create). */
 const char *pbvd_supported(void);
 
 const char *pbvd_strerror(int code);
+/* Build (NVRTC) the kernels pbvd_create would JIT for (K, R, polys) with
+ * `lanes` lanes per block pair (0 = default) and store them in the disk cache,
+ * without touching a GPU -- e.g. to warm the cache ahead of time.  Returns
+ * PBVD_OK, PBVD_EINVAL (arguments as pbvd_create) or PBVD_EUNSUPPORTED (no
+ * such shape / compile failed; the reason is written to msg, msg_len bytes
+ * incl. the terminating 0, if msg is not NULL).  Codes listed by
+ * pbvd_supported() need no build. */
+int pbvd_jit_prebuild(int K, int R, const uint32_t *polys, int lanes, char *msg, size_t msg_len);
+
+/* Message of the last failure on h; for h == NULL, of the calling thread's
+ * last failed pbvd_create. */
 const char *pbvd_last_error(pbvd_t h);
 
 #ifdef __cplusplus

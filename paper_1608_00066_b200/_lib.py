@@ -11,6 +11,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libpbvd.so"
 
 PBVD_OK = 0
 PBVD_TERMINATED = 1
+PBVD_ALLOW_CATASTROPHIC = 2
 
 EXPORTS = (
     "pbvd_create", "pbvd_destroy", "pbvd_llr_count", "pbvd_stage_count", "pbvd_block_count",
@@ -18,7 +19,7 @@ EXPORTS = (
     "pbvd_set_fused", "pbvd_get_fused",
     "pbvd_set_workspace_limit", "pbvd_set_profiling", "pbvd_kernel_times", "pbvd_get_info",
     "pbvd_supported", "pbvd_strerror", "pbvd_last_error", "pbvd_probe_acs_peak",
-    "pbvd_probe_acs_balanced",
+    "pbvd_probe_acs_balanced", "pbvd_jit_prebuild",
 )
 
 
@@ -26,7 +27,8 @@ class PbvdInfo(ctypes.Structure):
     _fields_ = [("K", ctypes.c_int), ("R", ctypes.c_int), ("N", ctypes.c_int),
                 ("lanes", ctypes.c_int), ("D", ctypes.c_int), ("L", ctypes.c_int),
                 ("P", ctypes.c_int), ("dec_bytes_per_block", ctypes.c_int64),
-                ("span", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t)]
+                ("span", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t),
+                ("jit", ctypes.c_int)]
 
 
 _lib = None
@@ -82,6 +84,9 @@ def load(path: os.PathLike | None = None):
     L.pbvd_probe_acs_balanced.argtypes = [i32, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_double)]
     L.pbvd_probe_acs_balanced.restype = i32
+    L.pbvd_jit_prebuild.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_uint32), i32, cp,
+                                     ctypes.c_size_t]
+    L.pbvd_jit_prebuild.restype = i32
     L.pbvd_supported.argtypes = []
     L.pbvd_supported.restype = cp
     L.pbvd_strerror.argtypes = [i32]

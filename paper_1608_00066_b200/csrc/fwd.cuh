@@ -113,13 +113,17 @@ struct Cfg {
     static constexpr int MAXREG = PBVD_MAXREG;  // room for the unrolled stage state
     static constexpr int BPC = NWARP * BPW;   // blocks per CTA
     static constexpr int PPC = NWARP * PPW;   // pairs per CTA
-    static constexpr int T = V * (32 / V);    // stages per chunk = normalisation period
     // int16 headroom of the biased metric BM'(c) = BM(c) + 128R in [0, 255R]
     // (reading c-4): PMs start a chunk at <= M0 = max(S_HEAD, v*128R) and grow
     // by <= 255R per stage, so after k <= T stages every PM, every E + BM and
     // every decision operand E + BM_own - m_other lies within +-(M0 + T*255R),
-    // which must fit int16 (reading c-20)
-    static_assert(cmax(S_HEAD, V * 128 * R) + T * 255 * R <= 32767, "int16 headroom");
+    // which must fit int16 (reading c-20).  T = stages per chunk = the
+    // normalisation period: the largest multiple of v <= 32 that keeps it
+    // (32 for every R <= 3 code; 24 for R = 4)
+    static constexpr int M0 = cmax(S_HEAD, V * 128 * R);
+    static constexpr int T = V * (cmin(32, (32767 - M0) / (255 * R)) / V);
+    static_assert(T >= V, "normalisation period");
+    static_assert(M0 + T * 255 * R <= 32767, "int16 headroom");
     // raw window per block and chunk: the T*R soft bytes rounded out to
     // 16-byte vectors (+1 vector for the alignment superset)
     static constexpr int BOXB = ((T * R + 15) / 16) * 16 + 16;
@@ -130,10 +134,11 @@ struct Cfg {
     // transform item = (pair, G stages): G*R bytes = whole words per block
     static constexpr int G = (R % 4 == 0) ? 1 : (R % 2 == 0) ? 2 : 4;
     static constexpr int NG = (T + G - 1) / G;                  // groups per chunk
-    // operand row of a pair: T*LW words, padded by 32/PPW words so that the
-    // PPW rows start in distinct banks (conflict-free per-stage reads across
-    // pairs) and, for PPW <= 16, stay 8-byte aligned for the transform stores
-    static constexpr int LSTR = ((NG * G * LW + 31) / 32) * 32 + 32 / PPW;
+    // operand row of a pair: T*LW words, padded by max(32/PPW, LW) words so
+    // that the PPW rows start in distinct banks (conflict-free per-stage reads
+    // across pairs) and, for LW = 2 (8-byte per-stage reads) or PPW <= 16,
+    // stay 8-byte aligned
+    static constexpr int LSTR = ((NG * G * LW + 31) / 32) * 32 + cmax(32 / PPW, LW);
     // per warp: raw windows [2][BPW][RAWB], operands [2][PPW][LSTR], depunctured [BPW][RAWB]
     static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered

@@ -33,7 +33,6 @@ const std::vector<Variant>& variants() {
 }
 
 static std::mutex g_prep_mu;
-static std::vector<int> g_prepared;  // per (device, variant) flag
 
 }  // namespace pbvd
 
@@ -110,15 +109,42 @@ int64_t kept_before_h(const pbvd_s* h, int64_t s) {
 
 int ensure_prepared(pbvd_t h, const Variant* v) {
     std::lock_guard<std::mutex> lk(g_prep_mu);
-    const auto& vs = variants();
-    const size_t idx = size_t(h->device) * vs.size() + size_t(v - vs.data());
-    if (g_prepared.size() <= idx) g_prepared.resize(idx + 1, 0);
-    if (!g_prepared[idx]) {
-        cudaError_t e = v->prepare();
-        if (e != cudaSuccess) return cuda_fail(h, e, "cudaFuncSetAttribute");
-        g_prepared[idx] = 1;
+    const uint64_t bit = uint64_t(1) << (h->device & 63);
+    if (!(v->prepared & bit)) {
+        const std::pair<const void*, size_t> ks[3] = {
+            {v->k_fwd, v->smem_fwd}, {v->k_fused, v->smem_fused}, {v->k_tb, v->smem_tb}};
+        for (const auto& k : ks) {
+            cudaError_t e = cudaFuncSetAttribute(k.first, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(k.second));
+            if (e != cudaSuccess) return cuda_fail(h, e, "cudaFuncSetAttribute");
+        }
+        v->prepared |= bit;
     }
     return PBVD_OK;
+}
+
+// One launch of a variant's kernel (compiled function or JIT cudaKernel_t).
+// The traceback grid uses programmatic stream serialization (PDL): its CTAs
+// may be scheduled once every forward CTA has signalled
+// griddepcontrol.launch_dependents, and they wait (griddepcontrol.wait) for
+// the forward grid's memory before touching survivors.
+template <class Params>
+cudaError_t launch(const void* k, int grid, int nt, size_t smem, cudaStream_t s, const Params& p,
+                   bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(nt));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    if (pdl) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    void* args[1] = {const_cast<Params*>(&p)};
+    return cudaLaunchKernelExC(&cfg, k, args);
 }
 
 int ensure_buf(pbvd_t h, void** p, size_t* cap, size_t bytes) {
@@ -367,8 +393,9 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
             fp.dbg = dbg;
         }
 #endif
-        if (h->fused) v->fused(fgrid, stream, fp);
-        else v->fwd(fgrid, stream, fp);
+        cudaError_t le = h->fused ? launch(v->k_fused, fgrid, v->NT, v->smem_fused, stream, fp, false)
+                                  : launch(v->k_fwd, fgrid, v->NT, v->smem_fwd, stream, fp, false);
+        if (le != cudaSuccess) return cuda_fail(h, le, "forward kernel launch");
 #ifdef PBVD_EXP_TIMING
         if (dump) {
             std::vector<unsigned long long> hb(ndbg);
@@ -389,7 +416,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         if (!h->fused) {
             const int ev2 = record(h, stream);
             if (ev2 >= 0) cudaEventRecord(h->ev_pool[ev2], stream);
-            v->tb(tp.n_int_ctas + ne, stream, tp);
+            le = launch(v->k_tb, tp.n_int_ctas + ne, v->NT_TB, v->smem_tb, stream, tp, true);
+            if (le != cudaSuccess) return cuda_fail(h, le, "traceback kernel launch");
             if (ev2 >= 0) {
                 cudaEventRecord(h->ev_pool[ev2 + 1], stream);
                 h->ev_tb.push_back({ev2, ev2 + 1});
@@ -402,36 +430,68 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     return PBVD_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_period,
-                const uint8_t* punct, int D, int L, int soft_bits, unsigned flags, int device) {
-    if (!out) return PBVD_EINVAL;
-    *out = nullptr;
-    if (!polys || K < 3 || K > 9 || R < 2 || R > 4) return PBVD_EINVAL;
-    if (punct_period < 1 || punct_period > 16 || R * punct_period > 64) return PBVD_EINVAL;
-    if ((punct_period > 1) != (punct != nullptr)) return PBVD_EINVAL;
-    if (D < 8 || (D % 8) != 0 || L < 1 || D > (1 << 24) || L > (1 << 20)) return PBVD_EINVAL;
-    if (soft_bits < 1 || soft_bits > 8) return PBVD_EINVAL;
-    if (flags & ~PBVD_TERMINATED) return PBVD_EINVAL;
-    for (int r = 0; r < R; ++r)
-        if (polys[r] == 0 || polys[r] >= (1u << K)) return PBVD_EINVAL;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
-        cudaGetLastError();
-        return PBVD_ECUDA;
-    }
+// The variant that runs (K, R, polys) with `lanes` lanes per block pair (0 =
+// the code's default): a compiled one if any, else a JIT build (jit.cu).
+const Variant* select_variant(int K, int R, const uint32_t* polys, int lanes, std::string* why) {
     const Variant* best = nullptr;
     for (const auto& v : variants()) {
         if (v.K != K || v.R != R) continue;
         bool same = true;
         for (int r = 0; r < R; ++r) same &= (v.polys[r] == polys[r]);
         if (!same) continue;
-        if (!best || v.default_rank < best->default_rank) best = &v;
+        if (lanes == 0 ? (!best || v.default_rank < best->default_rank) : v.W == lanes) best = &v;
     }
-    if (!best) return PBVD_EUNSUPPORTED;
+    if (best) return best;
+    return jit_variant(K, R, polys, lanes == 0 ? default_lanes(K) : lanes, why);
+}
+
+thread_local std::string g_create_err;   // pbvd_last_error(NULL)
+
+int create_fail(int code, const std::string& msg) {
+    g_create_err = msg;
+    return code;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_period,
+                const uint8_t* punct, int D, int L, int soft_bits, unsigned flags, int device) {
+    g_create_err.clear();
+    if (!out) return create_fail(PBVD_EINVAL, "null handle pointer");
+    *out = nullptr;
+    if (!polys || K < 3 || K > 9 || R < 2 || R > 4)
+        return create_fail(PBVD_EINVAL, "need 3 <= K <= 9, 2 <= R <= 4 and a polynomial list");
+    if (punct_period < 1 || punct_period > 16 || R * punct_period > 64)
+        return create_fail(PBVD_EINVAL, "puncture period out of range");
+    if ((punct_period > 1) != (punct != nullptr))
+        return create_fail(PBVD_EINVAL, "puncture matrix must be given iff period > 1");
+    if (D < 8 || (D % 8) != 0 || L < 1 || D > (1 << 24) || L > (1 << 20))
+        return create_fail(PBVD_EINVAL, "need D >= 8, D % 8 == 0, L >= 1");
+    if (soft_bits < 1 || soft_bits > 8) return create_fail(PBVD_EINVAL, "soft_bits outside 1..8");
+    if (flags & ~(PBVD_TERMINATED | PBVD_ALLOW_CATASTROPHIC))
+        return create_fail(PBVD_EINVAL, "unknown flag");
+    uint32_t lead = 0, trail = 0;
+    for (int r = 0; r < R; ++r) {
+        if (polys[r] == 0 || polys[r] >= (1u << K))
+            return create_fail(PBVD_EINVAL, "generator polynomial outside [1, 2^K)");
+        lead |= (polys[r] >> (K - 1)) & 1u;
+        trail |= polys[r] & 1u;
+    }
+    // leading / trailing coefficient rule of new_code: without
+    // them the code's constraint length is not K; warning-class, overridable
+    if (!(lead && trail) && !(flags & PBVD_ALLOW_CATASTROPHIC))
+        return create_fail(PBVD_EINVAL, "no generator has the g_{K-1} (or g_0) tap; "
+                                        "pass PBVD_ALLOW_CATASTROPHIC to decode it anyway");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return create_fail(PBVD_ECUDA, "no such CUDA device");
+    }
+    std::string why;
+    const Variant* best = select_variant(K, R, polys, 0, &why);
+    if (!best) return create_fail(PBVD_EUNSUPPORTED, why);
     pbvd_s* h = new (std::nothrow) pbvd_s();
     if (!h) return PBVD_ENOMEM;
     h->device = device;
@@ -602,15 +662,9 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
 
 int pbvd_set_lanes(pbvd_t h, int lanes) {
     if (!h) return PBVD_EINVAL;
-    const Variant* best = nullptr;
-    for (const auto& v : variants()) {
-        if (v.K != h->K || v.R != h->R) continue;
-        bool same = true;
-        for (int r = 0; r < h->R; ++r) same &= (v.polys[r] == h->polys[r]);
-        if (!same) continue;
-        if (lanes == 0 ? (!best || v.default_rank < best->default_rank) : v.W == lanes) best = &v;
-    }
-    if (!best) return fail(h, PBVD_EUNSUPPORTED, "no kernel variant with that lane count");
+    std::string why;
+    const Variant* best = select_variant(h->K, h->R, h->polys, lanes, &why);
+    if (!best) return fail(h, PBVD_EUNSUPPORTED, why);
     h->var = best;
     return PBVD_OK;
 }
@@ -670,6 +724,7 @@ int pbvd_get_info(pbvd_t h, pbvd_info* info) {
     info->P = h->P;
     info->span = h->D + 2 * h->L;
     info->dec_bytes_per_block = int64_t(h->D + 2 * h->L) * (h->N / 8 > 0 ? h->N / 8 : 1);
+    info->jit = h->var->jit ? 1 : 0;
     info->workspace_bytes = h->ws.bytes;
     for (const auto& ln : h->lanes) info->workspace_bytes += ln.ws.bytes;
     return PBVD_OK;
@@ -700,12 +755,12 @@ const char* pbvd_strerror(int code) {
         case PBVD_EINVAL: return "invalid argument";
         case PBVD_ENOMEM: return "out of memory";
         case PBVD_ECUDA: return "CUDA error";
-        case PBVD_EUNSUPPORTED: return "unsupported code (no compiled kernel)";
+        case PBVD_EUNSUPPORTED: return "unsupported code shape or lane count (no compiled or JIT kernel)";
         case PBVD_ESIZE: return "buffer size inconsistent with n_info";
         default: return "unknown error";
     }
 }
 
-const char* pbvd_last_error(pbvd_t h) { return h ? h->err.c_str() : "null handle"; }
+const char* pbvd_last_error(pbvd_t h) { return h ? h->err.c_str() : g_create_err.c_str(); }
 
 }  // extern "C"

@@ -18,8 +18,10 @@ def _check(rc, h=None, what=""):
     if rc < 0:
         L = _lib.load()
         msg = L.pbvd_strerror(rc).decode()
-        if h is not None:
-            msg += ": " + L.pbvd_last_error(h).decode()
+        # h None: the thread's last pbvd_create failure (pbvd_last_error(NULL))
+        detail = L.pbvd_last_error(h).decode()
+        if detail:
+            msg += ": " + detail
         raise PbvdError(f"{what} failed ({rc}): {msg}")
     return rc
 
@@ -31,6 +33,18 @@ def supported():
         K, R, polys, lanes = ent.split(":")
         out.append((int(K), int(R), tuple(int(p, 8) for p in polys.split(",")), int(lanes)))
     return out
+
+
+def jit_prebuild(K, polys, lanes=0):
+    """pbvd_jit_prebuild: NVRTC-build (no GPU needed) and disk-cache the kernels
+    pbvd_create would build at run time for a code that is not compiled in."""
+    L = _lib.load()
+    arr = (ctypes.c_uint32 * len(polys))(*[int(p) for p in polys])
+    msg = ctypes.create_string_buffer(8192)
+    rc = L.pbvd_jit_prebuild(int(K), len(polys), arr, int(lanes), msg, len(msg))
+    if rc < 0:
+        raise PbvdError(f"pbvd_jit_prebuild failed ({rc}): {L.pbvd_strerror(rc).decode()}: "
+                        f"{msg.value.decode(errors='replace')}")
 
 
 def probe_acs_balanced(device: int = 0):
@@ -59,7 +73,7 @@ class Decoder:
     punct: None or an R x P keep matrix (rows in generator order)."""
 
     def __init__(self, K, polys, D, L, punct=None, soft_bits=8, terminated=True, device=0,
-                 lanes=0, fused=True):
+                 lanes=0, fused=True, allow_catastrophic=False):
         self._L = _lib.load()
         self.K, self.polys, self.D, self.L = int(K), tuple(int(p) for p in polys), int(D), int(L)
         self.R = len(self.polys)
@@ -75,7 +89,9 @@ class Decoder:
             pp = (ctypes.c_uint8 * len(flat))(*flat)
         h = ctypes.c_void_p()
         rc = self._L.pbvd_create(ctypes.byref(h), self.K, self.R, arr, P, pp, self.D, self.L,
-                                 int(soft_bits), _lib.PBVD_TERMINATED if terminated else 0,
+                                 int(soft_bits),
+                                 (_lib.PBVD_TERMINATED if terminated else 0)
+                                 | (_lib.PBVD_ALLOW_CATASTROPHIC if allow_catastrophic else 0),
                                  self.device)
         _check(rc, None, "pbvd_create")
         self._h = h
