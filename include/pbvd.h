@@ -143,6 +143,38 @@ int pbvd_decode_host(pbvd_t h, const int8_t *h_llr_window, int64_t window_stage0
                      int64_t window_n_llr, int64_t n_info_total, int64_t block0,
                      int64_t nblocks, uint8_t *h_bits, int n_streams);
 
+/* Continuous stream (halo carry across calls; the SDR use case of P:424).
+ * A pbvd_stream_t belongs to one decoder handle and decodes ONE stream whose
+ * soft values arrive in pieces of any length (a piece may end inside a
+ * stage).  Each push appends d_llr (device, n_llr kept values in stream
+ * order, as in pbvd_decode) and decodes every block whose forward span
+ * [bD-L, bD+D+L) has fully arrived and which cannot be the last block,
+ * writing their bits to d_bits (device, bits_cap bytes; whole blocks, so a
+ * multiple of D bits) and the number of bits to *n_bits (0 if none is ready).
+ * pbvd_stream_finish ends the stream: the remaining blocks (including the
+ * last, traced back from state 0 if the handle is TERMINATED) are decoded to
+ * d_bits and *n_bits = n_info - bits emitted before, where n_info = stages
+ * received - (K-1 if TERMINATED).  The concatenation of all outputs equals
+ * pbvd_decode of the concatenated soft values, bit for bit.  After finish the
+ * object is empty and can take a new stream.  The soft values later blocks
+ * still need (L stages of halo plus the unfinished block) are carried in
+ * device buffers owned by the stream object, so the caller may reuse d_llr
+ * once the push's work on `stream` is done.  All calls on one stream object
+ * must use the same CUDA stream (or be ordered by the caller); the handle's
+ * workspace is shared, so do not decode on the handle concurrently.
+ * Errors: PBVD_EINVAL (null/negative), PBVD_ESIZE from a push whose ready
+ * blocks do not fit bits_cap (nothing is consumed; retry with a larger
+ * buffer -- (received stages / D + 1) * D bits always suffice) or from a
+ * finish whose stream ends inside a stage or has no info bit (the object is
+ * reset either way), PBVD_ENOMEM, PBVD_ECUDA. */
+typedef struct pbvd_stream_s *pbvd_stream_t;
+int pbvd_stream_open(pbvd_t h, pbvd_stream_t *out);
+int pbvd_stream_push(pbvd_stream_t s, const int8_t *d_llr, int64_t n_llr, uint8_t *d_bits,
+                     int64_t bits_cap, int64_t *n_bits, void *stream);
+int pbvd_stream_finish(pbvd_stream_t s, uint8_t *d_bits, int64_t bits_cap, int64_t *n_bits,
+                       void *stream);
+void pbvd_stream_close(pbvd_stream_t s);
+
 /* Tuning / introspection ------------------------------------------------- */
 
 /* Lanes per block pair used by the forward kernel (1, 2, 4, 8; 0 = default

@@ -20,6 +20,7 @@ EXPORTS = (
     "pbvd_set_workspace_limit", "pbvd_set_profiling", "pbvd_kernel_times", "pbvd_get_info",
     "pbvd_supported", "pbvd_strerror", "pbvd_last_error", "pbvd_probe_acs_peak",
     "pbvd_probe_acs_balanced", "pbvd_jit_prebuild",
+    "pbvd_stream_open", "pbvd_stream_push", "pbvd_stream_finish", "pbvd_stream_close",
 )
 
 
@@ -87,6 +88,14 @@ def load(path: os.PathLike | None = None):
     L.pbvd_jit_prebuild.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_uint32), i32, cp,
                                      ctypes.c_size_t]
     L.pbvd_jit_prebuild.restype = i32
+    L.pbvd_stream_open.argtypes = [h, ctypes.POINTER(h)]
+    L.pbvd_stream_open.restype = i32
+    L.pbvd_stream_push.argtypes = [h, vp, i64, vp, i64, ctypes.POINTER(i64), vp]
+    L.pbvd_stream_push.restype = i32
+    L.pbvd_stream_finish.argtypes = [h, vp, i64, ctypes.POINTER(i64), vp]
+    L.pbvd_stream_finish.restype = i32
+    L.pbvd_stream_close.argtypes = [h]
+    L.pbvd_stream_close.restype = None
     L.pbvd_supported.argtypes = []
     L.pbvd_supported.restype = cp
     L.pbvd_strerror.argtypes = [i32]

@@ -660,6 +660,154 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
     return rc;
 }
 
+// ---- continuous stream (the SDR use case) --------
+// Soft values arrive in pieces of any length; every block whose forward span
+// [bD-L, bD+D+L) has fully arrived (and which provably is not the last block)
+// is decoded as soon as its data is there, with exactly the geometry the
+// one-shot decode of the concatenated stream gives it, so the
+// concatenated output equals pbvd_decode's.  The soft values a later block
+// still needs (its L-stage halo) are carried over in a device window.
+
+struct pbvd_stream_s {
+    pbvd_t h = nullptr;
+    int8_t* buf[2] = {nullptr, nullptr};
+    size_t cap[2] = {0, 0};
+    int cur = 0;
+    int64_t win_stage0 = 0;   // buf[cur][0] = first kept value of this stage
+    int64_t kwin0 = 0;        // = kept_before(win_stage0)
+    int64_t received = 0;     // kept values pushed so far
+    int64_t next_block = 0;   // first block not yet emitted
+};
+
+namespace {
+
+// complete stages among the first k kept soft values
+int64_t stages_complete(const pbvd_s* h, int64_t k) {
+    if (h->P == 1) return k / h->R;
+    const int64_t full = k / h->kp, rem = k % h->kp;
+    int p = 0;
+    while (p + 1 < h->P && h->cum[p + 1] <= rem) ++p;
+    // column p is complete iff all its kept values arrived
+    const int kept_p = (p + 1 < h->P ? h->cum[p + 1] : h->kp) - h->cum[p];
+    const int64_t in_period = (rem - h->cum[p] >= kept_p) ? p + 1 : p;
+    return full * h->P + in_period;
+}
+
+}  // namespace
+
+int pbvd_stream_open(pbvd_t h, pbvd_stream_t* out) {
+    if (!h || !out) return PBVD_EINVAL;
+    *out = new (std::nothrow) pbvd_stream_s();
+    if (!*out) return PBVD_ENOMEM;
+    (*out)->h = h;
+    return PBVD_OK;
+}
+
+void pbvd_stream_close(pbvd_stream_t s) {
+    if (!s) return;
+    {
+        DeviceGuard g(s->h->device);
+        for (auto* b : s->buf)
+            if (b) cudaFree(b);
+    }
+    delete s;
+}
+
+int pbvd_stream_push(pbvd_stream_t s, const int8_t* d_llr, int64_t n_llr, uint8_t* d_bits,
+                     int64_t bits_cap, int64_t* n_bits, void* stream) {
+    if (!s || n_llr < 0 || (n_llr > 0 && !d_llr) || !n_bits) return PBVD_EINVAL;
+    pbvd_t h = s->h;
+    *n_bits = 0;
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t D = h->D, tailv = (h->flags & PBVD_TERMINATED) ? h->V : 0;
+    // blocks b with (b+1)D + max(L, tail+1) <= received stages: the whole span
+    // has arrived and b is not the last block (n_info > (b+1)D)
+    const int64_t st_rx = stages_complete(h, s->received + n_llr);
+    const int64_t margin = std::max<int64_t>(h->L, tailv + 1);
+    const int64_t ready = std::max(s->next_block, st_rx >= margin ? (st_rx - margin) / D : 0);
+    const int64_t nbits = (ready - s->next_block) * D;
+    if (nbits > 0 && (!d_bits || bits_cap * 8 < nbits))
+        return fail(h, PBVD_ESIZE, "stream output buffer too small (nothing consumed)");
+    // carry: the soft values from the first stage a pending block reads
+    const int64_t s0 = std::max<int64_t>(0, s->next_block * D - h->L);
+    const int64_t k0 = kept_before_h(h, s0);
+    const int64_t keep_n = s->received - k0;            // retained values
+    const size_t need = size_t(keep_n + n_llr);
+    if (need > 0) {
+        const bool in_place = (k0 == s->kwin0) && s->cap[s->cur] >= need && s->buf[s->cur];
+        if (!in_place) {
+            const int nx = 1 - s->cur;
+            if (s->cap[nx] < need) {
+                int rc = ensure_buf(h, reinterpret_cast<void**>(&s->buf[nx]), &s->cap[nx],
+                                    std::max(need, s->cap[nx] + s->cap[nx] / 2));
+                if (rc) return rc;
+            }
+            if (keep_n > 0) {
+                cudaError_t e = cudaMemcpyAsync(s->buf[nx], s->buf[s->cur] + (k0 - s->kwin0),
+                                                size_t(keep_n), cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) return cuda_fail(h, e, "stream carry copy");
+            }
+            s->cur = nx;
+            s->kwin0 = k0;
+            s->win_stage0 = s0;
+        }
+        if (n_llr > 0) {
+            cudaError_t e = cudaMemcpyAsync(s->buf[s->cur] + (s->received - s->kwin0), d_llr,
+                                            size_t(n_llr), cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(h, e, "stream append copy");
+        }
+    }
+    s->received += n_llr;
+    if (nbits == 0) return PBVD_OK;
+    // the geometry of these blocks is the same for any n_info > ready*D: use
+    // the stages received so far
+    h->ev_fwd.clear();
+    h->ev_tb.clear();
+    h->launches = 0;
+    int rc = run_blocks(h, h->ws, s->buf[s->cur], s->win_stage0, s->received - s->kwin0,
+                        st_rx - tailv, s->next_block, ready - s->next_block, d_bits, st);
+    if (rc) return rc;
+    s->next_block = ready;
+    *n_bits = nbits;
+    return PBVD_OK;
+}
+
+int pbvd_stream_finish(pbvd_stream_t s, uint8_t* d_bits, int64_t bits_cap, int64_t* n_bits,
+                       void* stream) {
+    if (!s || !n_bits) return PBVD_EINVAL;
+    pbvd_t h = s->h;
+    *n_bits = 0;
+    DeviceGuard g(h->device);
+    const int64_t tailv = (h->flags & PBVD_TERMINATED) ? h->V : 0;
+    const int64_t n_stages = stages_complete(h, s->received);
+    const int64_t n_info = n_stages - tailv;
+    int rc = PBVD_OK;
+    if (kept_before_h(h, n_stages) != s->received || n_info < 1) {
+        rc = fail(h, PBVD_ESIZE, "stream ends inside a stage or holds no info bit");
+    } else {
+        const int64_t nb = (n_info + h->D - 1) / h->D;
+        const int64_t nbits = n_info - s->next_block * h->D;
+        if (nbits > 0) {
+            if (!d_bits || bits_cap < (nbits + 7) / 8) {
+                rc = fail(h, PBVD_ESIZE, "stream output buffer too small");
+            } else {
+                h->ev_fwd.clear();
+                h->ev_tb.clear();
+                h->launches = 0;
+                rc = run_blocks(h, h->ws, s->buf[s->cur], s->win_stage0, s->received - s->kwin0,
+                                n_info, s->next_block, nb - s->next_block, d_bits,
+                                static_cast<cudaStream_t>(stream));
+                if (!rc) *n_bits = nbits;
+            }
+        }
+    }
+    // the stream object is ready for the next stream (buffers kept)
+    s->cur = 0;
+    s->win_stage0 = s->kwin0 = s->received = s->next_block = 0;
+    return rc;
+}
+
 int pbvd_set_lanes(pbvd_t h, int lanes) {
     if (!h) return PBVD_EINVAL;
     std::string why;

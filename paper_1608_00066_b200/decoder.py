@@ -168,6 +168,10 @@ class Decoder:
         return out
 
     # ------------------------------------------------------------- tuning
+    def open_stream(self) -> "StreamDecoder":
+        """pbvd_stream_open: a continuous-stream decoder on this handle."""
+        return StreamDecoder(self)
+
     def set_lanes(self, lanes: int):
         _check(self._L.pbvd_set_lanes(self._h, int(lanes)), self._h, "pbvd_set_lanes")
 
@@ -220,3 +224,72 @@ class Decoder:
 
     def __exit__(self, *exc):
         self.close()
+
+
+class StreamDecoder:
+    """pbvd_stream_*: decode one stream whose soft values arrive in pieces.
+
+    push(llr) returns the packed bits of every block completed by this piece
+    (a CUDA uint8 tensor, possibly empty); finish() returns the rest.  Their
+    concatenation equals Decoder.decode of the whole stream."""
+
+    def __init__(self, dec: Decoder):
+        self._dec, self._L = dec, dec._L
+        h = ctypes.c_void_p()
+        _check(self._L.pbvd_stream_open(dec._h, ctypes.byref(h)), dec._h, "pbvd_stream_open")
+        self._s = h
+        self._rx = 0          # kept soft values pushed
+        self._emitted = 0     # bits returned so far
+        R, punct = dec.R, dec.punct
+        if punct is None:
+            self._P, self._cum, self._kp = 1, [0], R
+        else:
+            self._P = len(punct[0])
+            self._cum, k = [], 0
+            for p in range(self._P):
+                self._cum.append(k)
+                k += sum(int(punct[r][p] != 0) for r in range(R))
+            self._kp = k
+
+    def _stages(self, k):
+        """Complete stages among the first k kept values (upper bound on bits)."""
+        full, rem = divmod(k, self._kp)
+        return full * self._P + sum(1 for p in range(1, self._P + 1)
+                                    if (self._cum[p] if p < self._P else self._kp) <= rem)
+
+    def _out(self, n_more, device):
+        nbits = max(0, self._stages(self._rx + n_more) - self._emitted)
+        return torch.empty((nbits + 7) // 8 + 1, dtype=torch.uint8, device=device)
+
+    def push(self, llr: torch.Tensor, stream=None) -> torch.Tensor:
+        if llr.dtype != torch.int8 or not llr.is_cuda or not llr.is_contiguous():
+            raise ValueError("llr must be a contiguous int8 CUDA tensor")
+        out = self._out(llr.numel(), llr.device)
+        n = ctypes.c_int64()
+        rc = self._L.pbvd_stream_push(self._s, llr.data_ptr(), llr.numel(), out.data_ptr(),
+                                      out.numel(), ctypes.byref(n), self._dec._stream(stream))
+        _check(rc, self._dec._h, "pbvd_stream_push")
+        self._rx += llr.numel()
+        self._emitted += n.value
+        return out[: n.value // 8]
+
+    def finish(self, stream=None):
+        """-> (packed bits of the remaining blocks, their bit count)."""
+        out = self._out(0, torch.device("cuda", self._dec.device))
+        n = ctypes.c_int64()
+        rc = self._L.pbvd_stream_finish(self._s, out.data_ptr(), out.numel(), ctypes.byref(n),
+                                        self._dec._stream(stream))
+        self._rx = self._emitted = 0
+        _check(rc, self._dec._h, "pbvd_stream_finish")
+        return out[: (n.value + 7) // 8], n.value
+
+    def close(self):
+        if getattr(self, "_s", None):
+            self._L.pbvd_stream_close(self._s)
+            self._s = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
