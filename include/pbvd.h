@@ -211,6 +211,11 @@ typedef struct {
     int64_t span;                /* forward stages of one interior block   */
     size_t workspace_bytes;      /* currently allocated                    */
     int jit;                     /* 1 if the kernels were built at run time */
+    int host_lanes;              /* lanes of the variant pbvd_decode_host uses:
+                                    the compiled one with the most lanes per
+                                    pair (>= 16 states per lane; lowest
+                                    per-warp latency -- that pipeline is
+                                    PCIe-bound) unless pbvd_set_lanes fixed it */
 } pbvd_info;
 int pbvd_get_info(pbvd_t h, pbvd_info *info);
 

@@ -29,7 +29,7 @@ class PbvdInfo(ctypes.Structure):
                 ("lanes", ctypes.c_int), ("D", ctypes.c_int), ("L", ctypes.c_int),
                 ("P", ctypes.c_int), ("dec_bytes_per_block", ctypes.c_int64),
                 ("span", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t),
-                ("jit", ctypes.c_int)]
+                ("jit", ctypes.c_int), ("host_lanes", ctypes.c_int)]
 
 
 _lib = None

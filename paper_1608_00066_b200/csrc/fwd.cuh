@@ -78,6 +78,12 @@
 #ifndef PBVD_FMA_SPLIT
 #define PBVD_FMA_SPLIT 1
 #endif
+#ifndef PBVD_PACK_IMAD
+#define PBVD_PACK_IMAD 0
+#endif
+#ifndef PBVD_DMIX
+#define PBVD_DMIX 0
+#endif
 
 namespace pbvd {
 
@@ -289,6 +295,18 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
                 w4[i] = (w2[2 * i] & M) | (w2[2 * i + 1] & ~M);
             }
             words[kw] = ((w4[0] & 0x0F0F0F0Fu) | (w4[1] & 0xF0F0F0F0u)) ^ inv;
+#elif PBVD_PACK_IMAD
+            // P_m: bytes 0x00/0xFF (signs as below).  sum_m 2^m P_m = 255 X where
+            // byte j of X has bit m = sign byte j of P_m, so X = sum_m P_m *
+            // (2^m / 255 mod 2^32): 8 IMADs on the FMA pipe instead of 7 LOP3s
+            // on the ALU pipe (1/255 mod 2^32 = 0xFEFEFEFF)
+            uint32_t acc = 0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const uint32_t pm = prmt(t[16 * kw + m], t[16 * kw + 8 + m], SEL);
+                acc = imad(pm, 0xFEFEFEFFu << m, acc);
+            }
+            words[kw] = acc ^ inv;
 #else
             // P_m: bytes = sign of [t(m).A, t(8+m).A, t(m).B, t(8+m).B] (0x00/0xFF);
             // bit m of every byte from P_m by a chain of LOP3 merges
@@ -351,6 +369,12 @@ __host__ __device__ constexpr bool fma_out(int k) {
     return PBVD_FMA_SPLIT == 0 ? false : PBVD_FMA_SPLIT == 1 ? (k & 1) != 0 : (k % 3) != 0;
 }
 
+// butterfly k (lower index) of phase P uses the IADD3 decision operands
+__host__ __device__ constexpr bool dmix_iadd3(int k, int P) {
+    // rank of k among the butterflies of the stage (k with bit P cleared)
+    return PBVD_DMIX > 0 && ((((k >> (P + 1)) << P) | (k & ((1 << P) - 1))) % 4) < PBVD_DMIX;
+}
+
 template <class CF, int P>
 __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
                                           int lg, uint32_t* drow, bool st, uint32_t one,
@@ -385,11 +409,18 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             const uint32_t nE = __viaddmin_s16x2(E, Pv[a], mO0);
             const uint32_t mO1 = add32(O, Pv[a ^ gK ^ g0]);
             const uint32_t nO = __viaddmin_s16x2(E, Pv[a ^ gK], mO1);
-            const uint32_t d = imad(O, neg1, E);
             pm[k] = nE;
             pm[k | pb] = nO;
-            t[k] = add32(d, KC[a]);
-            t[k | pb] = add32(d, KC[a ^ gK]);
+            // butterfly index within the stage: the first PBVD_DMIX of every 4
+            // take one IADD3 per output (ALU) instead of the shared-d pair
+            if (dmix_iadd3(k, P)) {
+                t[k] = sub_add(E, mO0, PC[a]);
+                t[k | pb] = sub_add(E, mO1, PC[a ^ gK]);
+            } else {
+                const uint32_t d = imad(O, neg1, E);
+                t[k] = add32(d, KC[a]);
+                t[k | pb] = add32(d, KC[a ^ gK]);
+            }
         }
         pack_store<CF>(t, 0u, drow, st);
         return;

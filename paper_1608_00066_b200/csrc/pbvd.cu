@@ -67,6 +67,11 @@ struct pbvd_s {
     int D = 0, L = 0, soft_bits = 8;
     unsigned flags = 0;
     const Variant* var = nullptr;
+    // variant of the host pipeline (pbvd_decode_host): PCIe-bound, so what
+    // counts is the latency of the segment decoded after the last copy --
+    // the compiled variant with the most lanes per pair (fewest states per
+    // lane, >= 16) unless the caller fixed the lane count
+    const Variant* host_var = nullptr;
     Workspace ws;
     size_t ws_limit = size_t(4) << 30;
     std::vector<HostLane> lanes;
@@ -445,6 +450,20 @@ const Variant* select_variant(int K, int R, const uint32_t* polys, int lanes, st
     return jit_variant(K, R, polys, lanes == 0 ? default_lanes(K) : lanes, why);
 }
 
+// The host pipeline's variant (see pbvd_s::host_var): among the COMPILED
+// variants of the code (no extra JIT build), the one with the most lanes per
+// pair that keeps >= 16 states per lane; else `dflt`.
+const Variant* latency_variant(int K, int R, const uint32_t* polys, const Variant* dflt) {
+    const Variant* best = dflt;
+    for (const auto& v : variants()) {
+        if (v.K != K || v.R != R || (1 << (K - 1)) / v.W < 16) continue;
+        bool same = true;
+        for (int r = 0; r < R; ++r) same &= (v.polys[r] == polys[r]);
+        if (same && v.W > best->W) best = &v;
+    }
+    return best;
+}
+
 thread_local std::string g_create_err;   // pbvd_last_error(NULL)
 
 int create_fail(int code, const std::string& msg) {
@@ -492,6 +511,7 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
     std::string why;
     const Variant* best = select_variant(K, R, polys, 0, &why);
     if (!best) return create_fail(PBVD_EUNSUPPORTED, why);
+    const Variant* hbest = latency_variant(K, R, polys, best);
     pbvd_s* h = new (std::nothrow) pbvd_s();
     if (!h) return PBVD_ENOMEM;
     h->device = device;
@@ -506,6 +526,7 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
     h->soft_bits = soft_bits;
     h->flags = flags;
     h->var = best;
+    h->host_var = hbest;
     if (punct_period > 1) {
         int kp = 0;
         for (int p = 0; p < punct_period; ++p) {
@@ -605,6 +626,8 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
     h->launches = 0;
     const bool prof = h->prof;
     h->prof = false;                       // events are per caller stream only
+    const Variant* var_saved = h->var;
+    h->var = h->host_var;
     const int64_t kb0 = kept_before_h(h, window_stage0);
     // segments: enough of them to overlap copies with kernels, each large
     // enough to keep the GPU busy on its own
@@ -616,6 +639,7 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
         HostLane ln;
         if (cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking) != cudaSuccess) {
             h->prof = prof;
+            h->var = var_saved;
             return cuda_fail(h, cudaGetLastError(), "cudaStreamCreate");
         }
         h->lanes.push_back(ln);
@@ -657,6 +681,7 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
         if (!rc && e != cudaSuccess) rc = cuda_fail(h, e, "decode (host pipeline)");
     }
     h->prof = prof;
+    h->var = var_saved;
     return rc;
 }
 
@@ -814,6 +839,7 @@ int pbvd_set_lanes(pbvd_t h, int lanes) {
     const Variant* best = select_variant(h->K, h->R, h->polys, lanes, &why);
     if (!best) return fail(h, PBVD_EUNSUPPORTED, why);
     h->var = best;
+    h->host_var = lanes == 0 ? latency_variant(h->K, h->R, h->polys, best) : best;
     return PBVD_OK;
 }
 
@@ -873,6 +899,7 @@ int pbvd_get_info(pbvd_t h, pbvd_info* info) {
     info->span = h->D + 2 * h->L;
     info->dec_bytes_per_block = int64_t(h->D + 2 * h->L) * (h->N / 8 > 0 ? h->N / 8 : 1);
     info->jit = h->var->jit ? 1 : 0;
+    info->host_lanes = h->host_var->W;
     info->workspace_bytes = h->ws.bytes;
     for (const auto& ln : h->lanes) info->workspace_bytes += ln.ws.bytes;
     return PBVD_OK;
