@@ -60,6 +60,21 @@ def parse():
 
 # ------------------------------------------------------------------ helpers
 
+def eq8_model(D, L, nblocks, U1, B, S_k, n_streams=3):
+    """The paper's Eq. 8 throughput model and its transfer-bound
+    counterpart for this pipeline (paper_1608_00066_b200/model.py), with the
+    segmentation pbvd_decode_host uses (nseg = min(2 n_streams, nblocks/8192),
+    pbvd.cu), the measured H2D rate B and S_k = the device-timed value."""
+    from paper_1608_00066_b200 import model as M
+    nseg = max(1, min(2 * n_streams, nblocks // 8192))
+    seg = -(-nblocks // nseg)
+    nseg = -(-nblocks // seg)
+    out = M.model(D, L, seg, nseg, U1, 1 / 8, B, S_k)
+    out["note"] = ("eq8 = Eq. 8 in its dimensionally consistent form (compute-bound premise); "
+                   "transfer_bound = every H2D batch on the critical path; model = min")
+    return out
+
+
 def workload(name, world):
     c = dict(synth.CONFIGS[name])
     c["name"] = name
@@ -487,6 +502,8 @@ def run_ours(args):
                "host_lanes": dec.info()["host_lanes"],
                "api": "pbvd_decode_host (pinned host buffers, 3 streams)",
                "matches_device_path": same,
+               "eq8": eq8_model(D, L, sh.nblocks, in_bytes / max(1, sh.stage1 - sh.stage0),
+                                llr_h.numel() / t_in, value * 1e9),
                "pcie": {"h2d_gbs": llr_h.numel() / t_in / 1e9, "d2h_gbs": out_h.numel() / t_out / 1e9,
                         "bound_value": bound, "frac_of_bound": e2e_v / bound}}
         del d_in, d_out
