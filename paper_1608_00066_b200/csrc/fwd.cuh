@@ -542,6 +542,8 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         unsigned smid; asm("mov.u32 %0, %%smid;" : "=r"(smid));
         p.dbg[8 * gw + 0] = gtime();
         p.dbg[8 * gw + 3] = smid;
+        unsigned wid; asm("mov.u32 %0, %%warpid;" : "=r"(wid));
+        p.dbg[8 * gw + 7] = wid;
     }
 #endif
     const int span = edge ? p.edges[e].span : p.span_int;

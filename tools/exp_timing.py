@@ -45,3 +45,18 @@ print("warps per SM histogram:", np.bincount(cnt))
 for k in sorted(set(cnt[sm])):
     sel = cnt[sm] == k
     print(f"  SMs with {k} warps: fwd dur p50 {np.percentile(fw[sel],50):.1f} max {fw[sel].max():.1f}; tb p50 {np.percentile(tb[sel],50):.1f}")
+
+# per SM sub-partition (%warpid % 4): warps sharing it vs their forward end
+wid = a[:, 7]
+key = sm * 4 + (wid % 4)
+kc = np.bincount(key, minlength=148 * 4)
+print("warps per sub-partition histogram:", np.bincount(kc))
+for k in sorted(set(kc[key])):
+    sel = kc[key] == k
+    print(f"  sub-partitions with {k} warps: fwd end p10 {np.percentile(fe[sel],10):.1f} p50 {np.percentile(fe[sel],50):.1f} "
+          f"p90 {np.percentile(fe[sel],90):.1f} max {fe[sel].max():.1f}; fwd dur p50 {np.percentile(fw[sel],50):.1f}")
+# among 2-warp sub-partitions: spread by SM warp count
+for k in sorted(set(cnt[sm])):
+    sel = (cnt[sm] == k) & (kc[key] == 2)
+    if sel.any():
+        print(f"  2-warp sub-partitions on SMs with {k} warps: fwd end p50 {np.percentile(fe[sel],50):.1f} max {fe[sel].max():.1f}")
