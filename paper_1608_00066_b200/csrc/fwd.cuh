@@ -84,6 +84,9 @@
 #ifndef PBVD_DMIX
 #define PBVD_DMIX 0
 #endif
+#ifndef PBVD_DEP_TABLE
+#define PBVD_DEP_TABLE 1
+#endif
 
 namespace pbvd {
 
@@ -618,6 +621,28 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         const int s0 = c * T;
         const int nst = min(T, span - s0);
         const uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
+#if PBVD_DEP_TABLE
+        // table-driven: every dense word is one funnel-shifted window word
+        // PRMT-ed with the (phase, word) selector of the host table -- all
+        // words independent (no serial kept-index chain)
+        constexpr int NWD = (T * R + 3) / 4;
+        for (int i = lane; i < nblk; i += 32) {
+            const int64_t a = block_lo(i) + s0;
+            const int woff = win_off(i, a);
+            const uint32_t* win = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(i) * RAWB);
+            const uint32_t* tab = p.dtab + int(a % p.P) * NWD;
+            const int nw = (nst * R + 3) / 4;
+#pragma unroll 4
+            for (int w = 0; w < nw; ++w) {
+                const uint32_t e = __ldg(tab + w);
+                const int q = woff + int(e >> 16);
+                const uint32_t x = __funnelshift_r(win[q >> 2], win[(q >> 2) + 1], uint32_t(q & 3) * 8u);
+                dst[w] = prmt(x, 0u, e & 0xffffu);
+            }
+        }
+        return;
+#endif
         for (int i = lane; i < nblk; i += 32) {
             const int64_t a = block_lo(i) + s0;
             const uint8_t* src = rb + size_t(i) * RAWB + win_off(i, a);

@@ -39,6 +39,10 @@ struct FwdParams {
     int kp;                // kept values per period
     uint64_t keep;         // keep flag of (r, p) at bit r*P + p
     int cum[16];           // kept values in columns [0, p) of one period
+    // depuncture table (P > 1): entry [ph0][w] for dense word w of a chunk
+    // starting at phase ph0 -- bits 0-15 a PRMT selector over the 4 kept
+    // bytes from bits 16-23 = first kept index of the word (nibble 4 = erasure)
+    const uint32_t* dtab;
     uint32_t* dec;         // interior survivor regions
     int32_t* start;        // interior start states (logical state index)
     uint32_t* dec_edge;    // edge survivor regions

@@ -64,6 +64,7 @@ struct pbvd_s {
     uint8_t punct[64] = {};
     int cum[16] = {};
     uint64_t keep = 0;
+    uint32_t* dtab = nullptr;   // device depuncture table (P > 1), see FwdParams::dtab
     int D = 0, L = 0, soft_bits = 8;
     unsigned flags = 0;
     const Variant* var = nullptr;
@@ -283,6 +284,7 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     fp.P = h->P;
     fp.kp = h->kp;
     fp.keep = h->keep;
+    fp.dtab = h->dtab;
     for (int i = 0; i < 16; ++i) fp.cum[i] = h->cum[i];
     fp.dec = dec_int;
     fp.start = start_int;
@@ -547,6 +549,41 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
         h->kp = R;
         h->keep = (uint64_t(1) << R) - 1;
     }
+    if (punct_period > 1) {
+        // depuncture table for the forward kernel (FwdParams::dtab): for a
+        // chunk of T stages starting at phase ph0, dense word w (bytes 4w..4w+3
+        // of the [stage][r] window) = PRMT(4 kept bytes from kept index base,
+        // 0, sel); erasures select a byte of the zero operand (c-18)
+        const int T = best->T, P = punct_period;
+        const int nwd = (T * R + 3) / 4;
+        std::vector<uint32_t> tab(size_t(P) * nwd);
+        for (int ph0 = 0; ph0 < P; ++ph0) {
+            std::vector<int> kidx(size_t(4) * nwd + 1), nextk(size_t(4) * nwd + 1);
+            int ki = 0;
+            for (int d = 0; d < 4 * nwd; ++d) {
+                const int st = d / R, r = d % R, ph = (ph0 + st) % P;
+                nextk[size_t(d)] = ki;
+                kidx[size_t(d)] = h->punct[r * P + ph] ? ki++ : -1;
+            }
+            for (int w = 0; w < nwd; ++w) {
+                int base = nextk[size_t(4 * w)];
+                uint32_t sel = 0;
+                for (int k = 0; k < 4; ++k) {
+                    const int ix = kidx[size_t(4 * w + k)];
+                    sel |= uint32_t(ix >= 0 ? ix - base : 4) << (4 * k);
+                }
+                tab[size_t(ph0) * nwd + w] = sel | (uint32_t(base) << 16);
+            }
+        }
+        DeviceGuard g(device);
+        if (cudaMalloc(&h->dtab, tab.size() * 4) != cudaSuccess ||
+            cudaMemcpy(h->dtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            if (h->dtab) cudaFree(h->dtab);
+            delete h;
+            return create_fail(PBVD_ENOMEM, "depuncture table");
+        }
+    }
     *out = h;
     return PBVD_OK;
 }
@@ -555,6 +592,7 @@ void pbvd_destroy(pbvd_t h) {
     if (!h) return;
     {
         DeviceGuard g(h->device);
+        if (h->dtab) cudaFree(h->dtab);
         if (h->ws.p) cudaFree(h->ws.p);
         if (h->ws.al) cudaFree(h->ws.al);
         for (auto& ln : h->lanes) {
