@@ -87,6 +87,9 @@
 #ifndef PBVD_DEP_TABLE
 #define PBVD_DEP_TABLE 1
 #endif
+#ifndef PBVD_WSLOT_HMAJOR
+#define PBVD_WSLOT_HMAJOR 1
+#endif
 
 namespace pbvd {
 
@@ -150,6 +153,13 @@ struct Cfg {
     static constexpr int LSTR = ((NG * G * LW + 31) / 32) * 32 + cmax(32 / PPW, LW);
     // per warp: raw windows [2][BPW][RAWB], operands [2][PPW][LSTR], depunctured [BPW][RAWB]
     static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
+    // window slot of block i in raw[.] / dep[]: even blocks first, then odd
+    // (h-major), so the PPW pairs' same-half windows are RAWB apart and a
+    // warp's 32-bit transform reads hit 8 banks instead of 4 (a 16-byte
+    // aligned window start can only reach banks = 0 mod 4)
+    __host__ __device__ static constexpr int wslot(int i) {
+        return PBVD_WSLOT_HMAJOR ? (i & 1) * PPW + (i >> 1) : i;
+    }
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
     // R = 2: the ACS loop reads each stage's two soft bytes of both blocks
@@ -579,7 +589,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             const int64_t a = block_lo(i) + s0;
             const int64_t k0 = kept_before(p, a, R) - p.kb_ws0;
             const uintptr_t ga = (vlo + uintptr_t(k0)) & ~uintptr_t(15);
-            uint8_t* dst = rb + size_t(i) * RAWB;
+            uint8_t* dst = rb + size_t(CF::wslot(i)) * RAWB;
             woffs[(c & 1) * BPW + i] = uint8_t((vlo + uintptr_t(k0)) & 15);
             if (ga >= vlo && ga + RAWB <= vhi) {
                 // interior fast path: a fixed number of 16-byte vectors
@@ -629,8 +639,8 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         for (int i = lane; i < nblk; i += 32) {
             const int64_t a = block_lo(i) + s0;
             const int woff = win_off(i, a);
-            const uint32_t* win = reinterpret_cast<const uint32_t*>(rb + size_t(i) * RAWB);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(i) * RAWB);
+            const uint32_t* win = reinterpret_cast<const uint32_t*>(rb + size_t(CF::wslot(i)) * RAWB);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(CF::wslot(i)) * RAWB);
             const uint32_t* tab = p.dtab + int(a % p.P) * NWD;
             const int nw = (nst * R + 3) / 4;
 #pragma unroll 4
@@ -645,8 +655,8 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
 #endif
         for (int i = lane; i < nblk; i += 32) {
             const int64_t a = block_lo(i) + s0;
-            const uint8_t* src = rb + size_t(i) * RAWB + win_off(i, a);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(i) * RAWB);
+            const uint8_t* src = rb + size_t(CF::wslot(i)) * RAWB + win_off(i, a);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(CF::wslot(i)) * RAWB);
             int ph = int(a % p.P), idx = 0, nb = 0;
             uint32_t acc = 0;
             for (int st = 0; st < nst; ++st) {
@@ -689,7 +699,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         for (int h = 0; h < 2; ++h) {
             const int i = edge ? 0 : 2 * tp + h;
             o0[h] = dense ? int(wo[i]) : 0;
-            base[h] = rb + size_t(i) * RAWB + (o0[h] & ~3);
+            base[h] = rb + size_t(CF::wslot(i)) * RAWB + (o0[h] & ~3);
             sh[h] = uint32_t(o0[h] & 3) * 8u;
         }
 #pragma unroll
@@ -795,8 +805,8 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             }
             const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
             const int iA = edge ? 0 : 2 * grp, iB = edge ? 0 : 2 * grp + 1;
-            src.a = rb + size_t(iA) * RAWB + (dense ? woffs[(c & 1) * BPW + iA] : 0);
-            src.b = rb + size_t(iB) * RAWB + (dense ? woffs[(c & 1) * BPW + iB] : 0);
+            src.a = rb + size_t(CF::wslot(iA)) * RAWB + (dense ? woffs[(c & 1) * BPW + iA] : 0);
+            src.b = rb + size_t(CF::wslot(iB)) * RAWB + (dense ? woffs[(c & 1) * BPW + iB] : 0);
         } else {
             // soft windows of chunk c+2 go in flight; those of chunk c+1 (issued a
             // chunk ago) must have landed before this chunk's transform slices
