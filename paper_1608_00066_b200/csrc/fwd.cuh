@@ -90,6 +90,9 @@
 #ifndef PBVD_WSLOT_HMAJOR
 #define PBVD_WSLOT_HMAJOR 1
 #endif
+#ifndef PBVD_CYCLE_PREFETCH
+#define PBVD_CYCLE_PREFETCH 1
+#endif
 
 namespace pbvd {
 
@@ -828,11 +831,22 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         uint32_t* drow = gdec + size_t(c) * T * ROW + size_t(lane) * CF::WPS;
         const int st_lo = s_read - c * T;     // rows below the traceback's first row: no store
         if (nst == T) {
+            // each cycle's first-stage operands are loaded one cycle ahead
+            // (within a cycle Cycle<> loads one stage ahead); the read past the
+            // chunk's last stage stays inside the operand row's padding
+            XY<CF> first = src.load(0);
 #pragma unroll 1
             for (int j = 0; j < CF::NCYC; ++j) {
                 const int s0 = j * V;
+#if PBVD_CYCLE_PREFETCH
+                const XY<CF> nfirst = src.load(s0 + V);
+                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, T, st_lo, first, p.one,
+                                        p.neg_one);
+                first = nfirst;
+#else
                 Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, T, st_lo, src.load(s0),
                                         p.one, p.neg_one);
+#endif
                 if constexpr (!CF::DIRECT) transform(c + 1, j);     // harmless past the last chunk
             }
         } else {
