@@ -63,6 +63,9 @@
 #ifndef PBVD_MAXREG
 #define PBVD_MAXREG 200
 #endif
+#ifndef PBVD_MAXREG_S64
+#define PBVD_MAXREG_S64 200
+#endif
 #ifndef PBVD_L2_HINTS
 #define PBVD_L2_HINTS 0
 #endif
@@ -125,7 +128,9 @@ struct Cfg {
     static constexpr int BPW = 2 * PPW;       // blocks per warp (= per survivor region)
     static constexpr int NWARP = 1;            // warps per CTA (each warp is autonomous)
     static constexpr int NT = NWARP * 32;
-    static constexpr int MAXREG = PBVD_MAXREG;  // room for the unrolled stage state
+    // room for the unrolled stage state; 64 states per lane (K = 9 with 4
+    // lanes, K = 7 with 1) hold twice the path metrics
+    static constexpr int MAXREG = S >= 64 ? PBVD_MAXREG_S64 : PBVD_MAXREG;
     static constexpr int BPC = NWARP * BPW;   // blocks per CTA
     static constexpr int PPC = NWARP * PPW;   // pairs per CTA
     // int16 headroom of the biased metric BM'(c) = BM(c) + 128R in [0, 255R]
