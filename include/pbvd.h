@@ -72,7 +72,7 @@ enum pbvd_status {
                                             tap (SPEC S:53-55 warning-class override) */
 
 /* Create a decoder on CUDA device `device`.
- *   K          constraint length, 3..9
+ *   K          constraint length, 3..12 (2^(K-1) states)
  *   R          generators per code (code rate 1/R before puncturing), 2..4
  *   polys      R generator polynomials (see Conventions); host pointer; each
  *              in [1, 2^K); some polynomial must have bit K-1 and some bit 0

@@ -884,13 +884,16 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
 
     // ---- traceback start: min PM, lowest logical state on ties --------
     const int pend = span % V;
+    // key = (PM << SB) | logical state: SB = max(8, v) bits of state (16 + 11 <= 32)
+    constexpr int SB = V > 8 ? V : 8;
+    constexpr uint32_t SMASK = (1u << SB) - 1u;
     uint32_t kA = 0xffffffffu, kB = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < S; ++k) {
         const uint32_t q = uint32_t(lg * S + k);
         const uint32_t u = ((q >> pend) | (q << (V - pend))) & uint32_t(N - 1);
-        kA = min(kA, ((pm[k] & 0xffffu) << 8) | u);
-        kB = min(kB, ((pm[k] >> 16) << 8) | u);
+        kA = min(kA, ((pm[k] & 0xffffu) << SB) | u);
+        kB = min(kB, ((pm[k] >> 16) << SB) | u);
     }
 #pragma unroll
     for (int o = 1; o < W; o <<= 1) {
@@ -908,11 +911,11 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             const int src = (i >> 1) * W;
             const uint32_t a = __shfl_sync(0xffffffffu, kA, src);
             const uint32_t b = __shfl_sync(0xffffffffu, kB, src);
-            stv[m] = ((i & 1) ? b : a) & 0xffu;
+            stv[m] = ((i & 1) ? b : a) & SMASK;
             ob[m] = p.out_bit0 + (wb0 + lane + 32 * m) * int64_t(p.D);
         }
         if (edge) {
-            stv[0] = (p.edges[e].flags & EDGE_START0) ? 0u : (__shfl_sync(0xffffffffu, kA, 0) & 0xffu);
+            stv[0] = (p.edges[e].flags & EDGE_START0) ? 0u : (__shfl_sync(0xffffffffu, kA, 0) & SMASK);
             ob[0] = p.edges[e].out_bit0;
         }
         const int nblk_tb = edge ? 1 : int(min(int64_t(BPW), int64_t(p.n_int) - wb0));
@@ -941,10 +944,10 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     if (lg == 0) {
         if (!edge) {
             const int64_t bi = wb0 + 2 * grp;
-            if (bi < p.n_int) p.start[bi] = int32_t(kA & 0xffu);
-            if (bi + 1 < p.n_int) p.start[bi + 1] = int32_t(kB & 0xffu);
+            if (bi < p.n_int) p.start[bi] = int32_t(kA & SMASK);
+            if (bi + 1 < p.n_int) p.start[bi + 1] = int32_t(kB & SMASK);
         } else if (grp == 0) {
-            p.start_edge[e] = (p.edges[e].flags & EDGE_START0) ? 0 : int32_t(kA & 0xffu);
+            p.start_edge[e] = (p.edges[e].flags & EDGE_START0) ? 0 : int32_t(kA & SMASK);
         }
     }
     pdl_launch_dependents();   // the traceback grid may start scheduling

@@ -1,5 +1,5 @@
 // jit.cu -- run-time kernels for codes with no compiled variant (SURVEY
-// §8(f) NEXT 4: any generator polynomials, K 3..9, R 2..4).
+// §8(f) NEXT 4: any generator polynomials, K 3..12, R 2..4).
 //
 // The forward / traceback kernels are templates on the code (the generator
 // columns fix the butterfly groups of Eqs. 3-6, at compile time,
@@ -48,9 +48,10 @@ using DummyCode = Code<K, R, (1u << (K - 1)) | 1u, (1u << (K - 1)) | 1u,
 
 // supported lane counts: S = N / W states per lane, at most 64 registers;
 // fewer than 16 states per lane (a survivor word shared by several lanes'
-// sub-words) only with one lane per pair, W <= 8
+// sub-words) only with one lane per pair, W <= 32 (K = 12: one block pair
+// per warp)
 constexpr bool shape_ok(int K, int W) {
-    return W >= 1 && W <= 8 && (1 << (K - 1)) / W >= 4 && (1 << (K - 1)) / W <= 64 &&
+    return W >= 1 && W <= 32 && (1 << (K - 1)) / W >= 4 && (1 << (K - 1)) / W <= 64 &&
            ((1 << (K - 1)) / W >= 16 || W == 1);
 }
 
@@ -71,6 +72,8 @@ bool shape_kr(int W, Variant* out) {
         case 2: return shape_w<K, R, 2>(out);
         case 4: return shape_w<K, R, 4>(out);
         case 8: return shape_w<K, R, 8>(out);
+        case 16: return shape_w<K, R, 16>(out);
+        case 32: return shape_w<K, R, 32>(out);
         default: return false;
     }
 }
@@ -96,11 +99,15 @@ bool variant_shape(int K, int R, int W, Variant* out) {
         case 7: return shape_k<7>(R, W, out);
         case 8: return shape_k<8>(R, W, out);
         case 9: return shape_k<9>(R, W, out);
+        case 10: return shape_k<10>(R, W, out);
+        case 11: return shape_k<11>(R, W, out);
+        case 12: return shape_k<12>(R, W, out);
         default: return false;
     }
 }
 
-int default_lanes(int K) { return K <= 6 ? 1 : K <= 8 ? 2 : 4; }
+// 64 states per lane from K = 9 up (K = 7: 32, the measured best)
+int default_lanes(int K) { return K <= 6 ? 1 : K <= 8 ? 2 : (1 << (K - 1)) / 64; }
 
 // ---- NVRTC (dlopen) ----------------------------------------------------------
 
@@ -380,7 +387,7 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
 extern "C" int pbvd_jit_prebuild(int K, int R, const uint32_t* polys, int lanes, char* msg,
                                  size_t msg_len) {
     if (msg && msg_len) msg[0] = 0;
-    if (!polys || K < 3 || K > 9 || R < 2 || R > 4) return PBVD_EINVAL;
+    if (!polys || K < 3 || K > 12 || R < 2 || R > 4) return PBVD_EINVAL;
     for (int r = 0; r < R; ++r)
         if (polys[r] == 0 || polys[r] >= (1u << K)) return PBVD_EINVAL;
     const int W = lanes == 0 ? pbvd::default_lanes(K) : lanes;

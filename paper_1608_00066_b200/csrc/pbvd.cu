@@ -376,7 +376,7 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         fp.n_int_warps = int((cnt + v->BPW - 1) / v->BPW);
         fp.n_edge = ne;
         tp.n_int = fp.n_int;
-        tp.n_int_ctas = int((cnt + 127) / 128);
+        tp.n_int_ctas = int((cnt + v->NT_TB - 1) / v->NT_TB);
         tp.out_bit0 = (g.i0 - B0) * D;
         fp.out_bit0 = tp.out_bit0;
         fp.word_out = tp.word_out;
@@ -482,8 +482,8 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
     g_create_err.clear();
     if (!out) return create_fail(PBVD_EINVAL, "null handle pointer");
     *out = nullptr;
-    if (!polys || K < 3 || K > 9 || R < 2 || R > 4)
-        return create_fail(PBVD_EINVAL, "need 3 <= K <= 9, 2 <= R <= 4 and a polynomial list");
+    if (!polys || K < 3 || K > 12 || R < 2 || R > 4)
+        return create_fail(PBVD_EINVAL, "need 3 <= K <= 12, 2 <= R <= 4 and a polynomial list");
     if (punct_period < 1 || punct_period > 16 || R * punct_period > 64)
         return create_fail(PBVD_EINVAL, "puncture period out of range");
     if ((punct_period > 1) != (punct != nullptr))

@@ -35,7 +35,14 @@ namespace pbvd {
 
 template <class CF>
 struct TbCfg {
-    static constexpr int NT = 128;                          // blocks per CTA
+    // blocks per CTA: 128, fewer for codes whose survivor rows are so wide
+    // (K >= 11: 2 blocks per region, 512-byte rows) that a 3-deep ring of
+    // v-row chunks for 128 blocks would not fit in 96 KB
+    static constexpr bool fits(int nt) {
+        return 3 * (nt / CF::BPW) * CF::V * CF::ROW * 4 <= 98304;
+    }
+    static constexpr int NT = fits(128) ? 128 : fits(64) ? 64 : fits(32) ? 32 : fits(16) ? 16 : 8;
+    static_assert(NT >= CF::BPW, "traceback CTA holds whole regions");
     static constexpr int NR = NT / CF::BPW;                 // regions per CTA
     static constexpr int ROW = CF::ROW;                     // words per stage per region
     static constexpr int NBUF = 3;                          // ring depth (chunks)

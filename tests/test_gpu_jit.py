@@ -1,5 +1,5 @@
 """GPU parity of the run-time (NVRTC) kernels: codes that are not compiled
-into libpbvd.so (SURVEY §8(f) NEXT 4 -- any generator polynomials, K 3..9,
+into libpbvd.so (SURVEY §8(f) NEXT 4 -- any generator polynomials, K 3..12,
 R 2..4, degenerate groupings) decoded through the C ABI and compared with the
 CPU oracle bit for bit.  The oracle is code-generic (it evaluates Eq. 2,
 P:128-133, per edge), so these codes are pinned exactly like the compiled
@@ -24,6 +24,10 @@ JIT_CODES = [
     ("k8", 8, (0o247, 0o371), None, 512, 48, 9000, 3.0),                  # 128 states
     ("k3-r3", 3, (0o5, 0o7, 0o7), None, 64, 16, 6000, 2.0),               # rank-2 grouping (dup poly)
     ("k7-133-171-3/4", 7, (0o133, 0o171), ((1, 1, 0), (1, 0, 1)), 512, 42, 12000, 4.0),
+    ("k10", 10, (0o1467, 0o1751), None, 256, 50, 6000, 3.0),              # 512 states, 8 lanes
+    ("k11", 11, (0o3345, 0o3613), None, 256, 56, 5000, 3.0),              # 1024 states, 16 lanes
+    ("k12", 12, (0o5723, 0o6265), None, 256, 60, 5000, 3.0),              # 2048 states, a pair per warp
+    ("k12-r3", 12, (0o5723, 0o6265, 0o7173), None, 128, 60, 3000, 2.0),
 ]
 
 
@@ -58,7 +62,7 @@ def test_jit_code_bit_exact(pbvd, orc, case):
     code = {"K": K, "polys": polys}
     assert all(tuple(p) != polys for (k, r, p, w) in pbvd.supported() if k == K)
     with pytest.raises(pbvd.PbvdError, match="shape"):
-        pbvd.Decoder(K, polys, D, L, punct=punct, lanes=16)
+        pbvd.Decoder(K, polys, D, L, punct=punct, lanes=64)
     _check(pbvd, orc, code, punct, n_info, D, L, ebn0, 23)
     # unterminated stream with a partial last block
     _check(pbvd, orc, code, punct, n_info - 5, D, L, ebn0, 29, term=False)

@@ -24,7 +24,7 @@ def test_prebuild_compiles(L, K, polys):
 def test_prebuild_rejects(L):
     arr = (ctypes.c_uint32 * 2)(0o171, 0o133)
     msg = ctypes.create_string_buffer(256)
-    assert L.pbvd_jit_prebuild(10, 2, arr, 0, msg, 256) == -1          # K out of range
+    assert L.pbvd_jit_prebuild(13, 2, arr, 0, msg, 256) == -1          # K out of range
     assert L.pbvd_jit_prebuild(7, 2, arr, 16, msg, 256) == -4          # no 16-lane shape
     assert b"shape" in msg.value
     assert L.pbvd_jit_prebuild(7, 2, arr, 8, msg, 256) == -4           # 8 states per lane
