@@ -1,0 +1,62 @@
+"""bench.py contract on one GPU: the N = 1 JSON line, and the N > 1 control
+flow (block-range shards, barrier, max-over-ranks timing, final gather) with
+two torchrun ranks sharing cuda:0 over gloo (PBVD_BENCH_BACKEND=gloo; the
+real multi-GPU run uses NCCL)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches",
+        "clocks", "parity")
+
+
+def _line(out):
+    lines = [l for l in out.splitlines() if l.startswith("{")]
+    assert lines, out[-2000:]
+    return json.loads(lines[-1])
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_bench_single_gpu_contract(gpu):
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _line(r.stdout)
+    for k in KEYS:
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["parity"]["bit_exact"]
+    assert d["roofline"]["bound"] == "alu" and 0 < d["roofline"]["frac"] < 1
+    assert d["e2e"]["matches_device_path"] and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 3
+
+
+def test_bench_two_ranks_gloo(gpu):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, PBVD_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _line(r.stdout)
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["parity"]["bit_exact"]
+    assert "x2" in d["config"]["parallelism"]
