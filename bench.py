@@ -330,7 +330,41 @@ def run_ours(args):
     gathered = None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
+    # N > 1: the gather of the decoded bits (a10).  Default: fused into
+    # the traceback -- every rank's gather buffer is mapped into every other
+    # rank through CUDA IPC (peer access over NVLink) and the decode kernel
+    # stores each output word to all of them (pbvd_decode_blocks_mirrored);
+    # checked against an NCCL all_gather after the warm-up, with the NCCL
+    # all_gather as the fallback (PBVD_BENCH_GATHER=nccl forces it).
+    gather_mode = "none" if world == 1 else os.environ.get("PBVD_BENCH_GATHER", "peer")
+    gbuf, mirrors = None, []
+    if gather_mode == "peer":
+        ok = 1
+        try:
+            from torch.multiprocessing.reductions import reduce_tensor
+            total_bytes = (n_total + 7) // 8
+            gbuf = torch.zeros(total_bytes, dtype=torch.uint8, device=dev)
+            fn, fargs = reduce_tensor(gbuf)
+            all_args = [None] * world
+            dist.all_gather_object(all_args, fargs)
+            peer_bufs = [gbuf if r == rank else fn(*a) for r, a in enumerate(all_args)]
+            o = sh.bit0 // 8
+            mirrors = [peer_bufs[r].data_ptr() + o for r in range(world) if r != rank]
+            out = gbuf[o:o + sh.nbytes]
+        except Exception as ex:  # pragma: no cover - depends on the box
+            print(f"peer gather setup failed ({ex}); NCCL all_gather instead", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=cdev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            gather_mode = "nccl"
+            out = torch.empty(sh.nbytes, dtype=torch.uint8, device=dev)
+
     def step():
+        if gather_mode == "peer":
+            dec.decode_blocks_mirrored(llr, sh.stage0, n_total, sh.block0, sh.nblocks, out,
+                                       mirrors)
+            return gbuf
         dec.decode_blocks(llr, sh.stage0, n_total, sh.block0, sh.nblocks, out=out)
         if world > 1:
             return S.gather_bits(out.to(cdev), sh, n_total, D)
@@ -348,6 +382,18 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if gather_mode == "peer":
+        # every rank's buffer must now hold the whole stream: compare with an
+        # NCCL all_gather of this rank's own bits; any mismatch -> NCCL path
+        ref = S.gather_bits(out.clone().to(cdev), sh, n_total, D)
+        good = torch.tensor([int(torch.equal(ref.to(dev), gbuf))], dtype=torch.int32, device=cdev)
+        dist.all_reduce(good, op=dist.ReduceOp.MIN)
+        if not int(good.item()):
+            print("peer gather check failed; NCCL all_gather instead", file=sys.stderr)
+            gather_mode = "nccl"
+            out = out.clone()
+        torch.cuda.synchronize()
+        dist.barrier()
 
     stream = torch.cuda.current_stream(dev)
     times, launches = [], 0
@@ -527,7 +573,11 @@ def run_ours(args):
             "config": {"workload": describe(c, code, n_total, world),
                        "n_info_total": n_total, "D": D, "L": L, "lanes": dec.lanes,
                        "l2": "flushed (256 MiB memset) before every timed step",
-                       "parallelism": f"block-range shards x{world}"},
+                       "parallelism": f"block-range shards x{world}",
+                       "gather": {"none": "none (1 GPU)",
+                                  "peer": "fused into the traceback: stores to every rank's "
+                                          "buffer over CUDA IPC / NVLink",
+                                  "nccl": "NCCL all_gather"}[gather_mode]},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "parity": parity,
         }

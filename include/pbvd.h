@@ -129,6 +129,21 @@ int pbvd_decode_blocks(pbvd_t h, const int8_t *d_llr_window, int64_t window_stag
                        int64_t window_n_llr, int64_t n_info_total, int64_t block0,
                        int64_t nblocks, uint8_t *d_bits, void *stream);
 
+/* pbvd_decode_blocks whose decoded bits are ALSO stored, by the traceback
+ * itself, to n_mirrors (0..7) further destinations: d_mirrors[k] receives
+ * the same bytes as d_bits.  The destinations may be other GPUs' memory
+ * mapped into this process (CUDA IPC handles / peer access over NVLink), so a
+ * multi-GPU run gathers its output inside the decode kernel -- the "final
+ * gather" of P:112 fused with the traceback that produces the bits instead
+ * of a separate NCCL collective.  Each d_mirrors[k] must be congruent to
+ * d_bits modulo 4 (PBVD_EINVAL otherwise).  Completion on a destination
+ * device is the completion of this call's work on `stream` (synchronise or
+ * barrier before reading there).  Asynchronous on `stream`. */
+int pbvd_decode_blocks_mirrored(pbvd_t h, const int8_t *d_llr_window, int64_t window_stage0,
+                                int64_t window_n_llr, int64_t n_info_total, int64_t block0,
+                                int64_t nblocks, uint8_t *d_bits, uint8_t *const *d_mirrors,
+                                int n_mirrors, void *stream);
+
 /* End-to-end decode of blocks [block0, block0+nblocks) from HOST memory
  * (arguments as pbvd_decode_blocks, but h_llr_window / h_bits are host
  * pointers): the range is cut into segments that are copied to the device,

@@ -21,6 +21,7 @@ EXPORTS = (
     "pbvd_supported", "pbvd_strerror", "pbvd_last_error", "pbvd_probe_acs_peak",
     "pbvd_probe_acs_balanced", "pbvd_jit_prebuild",
     "pbvd_stream_open", "pbvd_stream_push", "pbvd_stream_finish", "pbvd_stream_close",
+    "pbvd_decode_blocks_mirrored",
 )
 
 
@@ -60,6 +61,9 @@ def load(path: os.PathLike | None = None):
     L.pbvd_decode.restype = i32
     L.pbvd_decode_blocks.argtypes = [h, vp, i64, i64, i64, i64, i64, vp, vp]
     L.pbvd_decode_blocks.restype = i32
+    L.pbvd_decode_blocks_mirrored.argtypes = [h, vp, i64, i64, i64, i64, i64, vp,
+                                              ctypes.POINTER(ctypes.c_void_p), i32, vp]
+    L.pbvd_decode_blocks_mirrored.restype = i32
     L.pbvd_decode_host.argtypes = [h, vp, i64, i64, i64, i64, i64, vp, i32]
     L.pbvd_decode_host.restype = i32
     L.pbvd_set_lanes.argtypes = [h, i32]

@@ -929,7 +929,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                            edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,
                            p.word_out && (!edge || (((ob[0] | int64_t(p.edges[e].t1r -
                                                                         p.edges[e].t0r)) & 31) == 0)),
-                           p.out, lane,
+                           p.out, p.mirror, p.n_mirror, lane,
 #ifdef PBVD_EXP_TIMING
                            p.dbg ? p.dbg + 8 * gw : nullptr);
 #else

@@ -78,6 +78,8 @@ struct pbvd_s {
     std::vector<HostLane> lanes;
     bool prof = false;
     bool fused = true;     // forward + in-warp traceback in one kernel (pbvd_set_fused)
+    int n_mirror = 0;      // extra output destinations of the current call (byte offsets)
+    int64_t mirror[MAX_MIRROR] = {};
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_fwd, ev_tb;   // indices into ev_pool
     int launches = 0;
@@ -292,6 +294,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     fp.start_edge = start_edge;
     fp.span_edge_max = span_edge_max;
     fp.out = out;
+    fp.n_mirror = h->n_mirror;
+    for (int k = 0; k < MAX_MIRROR; ++k) fp.mirror[k] = h->mirror[k];
     fp.t0r = int(L);
     fp.t1r = int(L + D);
 
@@ -303,6 +307,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     tp.t1r = int(L + D);
     tp.D = int(D);
     tp.out = out;
+    tp.n_mirror = h->n_mirror;
+    for (int k = 0; k < MAX_MIRROR; ++k) tp.mirror[k] = h->mirror[k];
     tp.dec_edge = dec_edge;
     tp.start_edge = start_edge;
     tp.span_edge_max = span_edge_max;
@@ -634,6 +640,25 @@ int pbvd_decode_blocks(pbvd_t h, const int8_t* d_llr_window, int64_t window_stag
     h->launches = 0;
     return run_blocks(h, h->ws, d_llr_window, window_stage0, window_n_llr, n_info_total, block0,
                       nblocks, d_bits, static_cast<cudaStream_t>(stream));
+}
+
+int pbvd_decode_blocks_mirrored(pbvd_t h, const int8_t* d_llr_window, int64_t window_stage0,
+                                int64_t window_n_llr, int64_t n_info_total, int64_t block0,
+                                int64_t nblocks, uint8_t* d_bits, uint8_t* const* d_mirrors,
+                                int n_mirrors, void* stream) {
+    if (!h) return PBVD_EINVAL;
+    if (n_mirrors < 0 || n_mirrors > MAX_MIRROR || (n_mirrors > 0 && !d_mirrors) || !d_bits)
+        return fail(h, PBVD_EINVAL, "0..7 mirror destinations");
+    for (int k = 0; k < n_mirrors; ++k) {
+        const int64_t d = reinterpret_cast<intptr_t>(d_mirrors[k]) - reinterpret_cast<intptr_t>(d_bits);
+        if (!d_mirrors[k] || (d & 3)) return fail(h, PBVD_EINVAL, "mirror null or not congruent to d_bits mod 4");
+        h->mirror[k] = d;
+    }
+    h->n_mirror = n_mirrors;
+    const int rc = pbvd_decode_blocks(h, d_llr_window, window_stage0, window_n_llr, n_info_total,
+                                      block0, nblocks, d_bits, stream);
+    h->n_mirror = 0;
+    return rc;
 }
 
 int pbvd_decode(pbvd_t h, const int8_t* d_llr, int64_t n_llr, uint8_t* d_bits, int64_t n_info,

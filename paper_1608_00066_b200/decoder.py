@@ -146,6 +146,22 @@ class Decoder:
         _check(rc, self._h, "pbvd_decode_blocks")
         return out
 
+    def decode_blocks_mirrored(self, llr_window: torch.Tensor, window_stage0: int,
+                               n_info_total: int, block0: int, nblocks: int, out: torch.Tensor,
+                               mirror_ptrs, stream=None) -> torch.Tensor:
+        """pbvd_decode_blocks_mirrored: decode_blocks whose traceback also stores
+        the bits at every address in mirror_ptrs (ints: device pointers, e.g.
+        other ranks' gather buffers opened through CUDA IPC)."""
+        if llr_window.dtype != torch.int8 or not llr_window.is_cuda:
+            raise ValueError("llr_window must be an int8 CUDA tensor")
+        arr = (ctypes.c_void_p * max(1, len(mirror_ptrs)))(*[int(x) for x in mirror_ptrs])
+        rc = self._L.pbvd_decode_blocks_mirrored(
+            self._h, llr_window.data_ptr(), int(window_stage0), llr_window.numel(),
+            int(n_info_total), int(block0), int(nblocks), out.data_ptr(), arr, len(mirror_ptrs),
+            self._stream(stream))
+        _check(rc, self._h, "pbvd_decode_blocks_mirrored")
+        return out
+
     def decode_host(self, llr: torch.Tensor, n_info: int, out: torch.Tensor | None = None,
                     n_streams: int = 3, window_stage0: int = 0, block0: int = 0,
                     nblocks: int | None = None) -> torch.Tensor:

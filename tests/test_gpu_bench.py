@@ -60,3 +60,32 @@ def test_bench_two_ranks_gloo(gpu):
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
     assert d["parity"]["bit_exact"]
     assert "x2" in d["config"]["parallelism"]
+    # the default gather: fused into the traceback over CUDA IPC, verified
+    # against an NCCL/gloo all_gather after the warm-up (else it falls back)
+    assert d["config"]["gather"].startswith("fused"), d["config"]["gather"]
+
+
+def test_mirrored_outputs_equal_plain_decode(gpu):
+    """pbvd_decode_blocks_mirrored: the traceback's stores land identically in
+    every destination (here: two more local buffers at odd 4-byte offsets),
+    for fused and two-kernel mode and a range with edge blocks."""
+    sys.path.insert(0, str(ROOT))
+    import synth
+    import paper_1608_00066_b200 as P
+    code = synth.CODES["k7"]
+    n_info, D, L = 100000, 512, 42
+    info, llr = synth.make_stream(code, n_info, 3.0, 61, device="cuda")
+    for fused in (True, False):
+        dec = P.Decoder(7, code["polys"], D, L, fused=fused)
+        want = dec.decode(llr, n_info)
+        nb = dec.block_count(n_info)
+        out = torch.zeros(want.numel(), dtype=torch.uint8, device="cuda")
+        m1 = torch.zeros(want.numel() + 4, dtype=torch.uint8, device="cuda")
+        m2 = torch.zeros(want.numel() + 8, dtype=torch.uint8, device="cuda")
+        dec.decode_blocks_mirrored(llr, 0, n_info, 0, nb, out,
+                                   [m1.data_ptr() + 4, m2.data_ptr() + 8])
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
+        assert torch.equal(m1[4:], want) and torch.equal(m2[8:], want)
+        with pytest.raises(P.PbvdError):       # not congruent mod 4
+            dec.decode_blocks_mirrored(llr, 0, n_info, 0, nb, out, [m1.data_ptr() + 1])
