@@ -134,8 +134,10 @@ int pbvd_decode_blocks(pbvd_t h, const int8_t *d_llr_window, int64_t window_stag
  * the same bytes as d_bits.  The destinations may be other GPUs' memory
  * mapped into this process (CUDA IPC handles / peer access over NVLink), so a
  * multi-GPU run gathers its output inside the decode kernel -- the "final
- * gather" of P:112 fused with the traceback that produces the bits instead
- * of a separate NCCL collective.  Each d_mirrors[k] must be congruent to
+ * gather" of P:112 fused with the traceback that produces the bits (each
+ * warp copies its blocks' bytes to the mirrors right after its walk, while
+ * other warps still compute) instead of a separate NCCL collective; in
+ * two-kernel mode (pbvd_set_fused(h, 0)) the copies follow the traceback.  Each d_mirrors[k] must be congruent to
  * d_bits modulo 4 (PBVD_EINVAL otherwise).  Completion on a destination
  * device is the completion of this call's work on `stream` (synchronise or
  * barrier before reading there).  Asynchronous on `stream`. */

@@ -538,7 +538,10 @@ __device__ __forceinline__ int64_t kept_before(const FwdParams& p, int64_t s, in
     return (s / p.P) * p.kp + p.cum[s % p.P];
 }
 
-template <class CF, bool FUSED>
+// MIRROR (fused only): after its walk each warp also copies its decoded bytes
+// to the p.mirror destinations (the multi-GPU gather, pbvd_decode_blocks_mirrored);
+// a separate instantiation so the default kernel carries none of that code
+template <class CF, bool FUSED, bool MIRROR = false>
 __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(const __grid_constant__ FwdParams p) {
     constexpr int V = CF::V, N = CF::N, S = CF::S, W = CF::W, R = CF::R, T = CF::T;
     constexpr int BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW, RAWB = CF::RAWB;
@@ -929,12 +932,27 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                            edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,
                            p.word_out && (!edge || (((ob[0] | int64_t(p.edges[e].t1r -
                                                                         p.edges[e].t0r)) & 31) == 0)),
-                           p.out, p.mirror, p.n_mirror, lane,
+                           p.out, lane,
 #ifdef PBVD_EXP_TIMING
                            p.dbg ? p.dbg + 8 * gw : nullptr);
 #else
                            nullptr);
 #endif
+        if constexpr (MIRROR) {
+            // multi-GPU gather fused into this kernel: the warp's decoded
+            // bytes (its blocks own whole, contiguous bytes) go to every
+            // mirror destination (other ranks' buffers over NVLink)
+            __syncwarp();          // the walk's stores of all lanes are visible
+            int64_t bit0, nbits;
+            if (!edge) {
+                bit0 = p.out_bit0 + wb0 * int64_t(p.D);
+                nbits = int64_t(nblk_tb) * p.D;
+            } else {
+                bit0 = p.edges[e].out_bit0;
+                nbits = p.edges[e].t1r - p.edges[e].t0r;
+            }
+            mirror_copy(p.out + (bit0 >> 3), (nbits + 7) >> 3, p.mirror, p.n_mirror, lane, 32);
+        }
 #ifdef PBVD_EXP_TIMING
         __syncwarp();
         if (p.dbg && lane == 0) p.dbg[8 * gw + 2] = gtime();

@@ -219,14 +219,14 @@ void mkdirs(const std::string& d) {
         if (k == d.size() || d[k] == '/') mkdir(d.substr(0, k).c_str(), 0755);
 }
 
-// cache file: "PBVDJIT1\n" + 3 lowered names (one per line) + cubin bytes
-constexpr char MAGIC[] = "PBVDJIT1\n";
+// cache file: "PBVDJIT2\n" + 4 lowered names (one per line) + cubin bytes
+constexpr char MAGIC[] = "PBVDJIT2\n";
 
-bool cache_load(const std::string& path, std::string names[3], std::string* cubin) {
+bool cache_load(const std::string& path, std::string names[4], std::string* cubin) {
     std::string all;
     if (!read_file(path, &all) || all.compare(0, sizeof MAGIC - 1, MAGIC) != 0) return false;
     size_t pos = sizeof MAGIC - 1;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
         const size_t e = all.find('\n', pos);
         if (e == std::string::npos) return false;
         names[i] = all.substr(pos, e - pos);
@@ -236,14 +236,14 @@ bool cache_load(const std::string& path, std::string names[3], std::string* cubi
     return !cubin->empty();
 }
 
-void cache_store(const std::string& dir, const std::string& path, const std::string names[3],
+void cache_store(const std::string& dir, const std::string& path, const std::string names[4],
                  const std::string& cubin) {
     mkdirs(dir);
     const std::string tmp = path + ".tmp" + std::to_string(getpid());
     {
         std::ofstream f(tmp, std::ios::binary);
         if (!f) return;
-        f << MAGIC << names[0] << '\n' << names[1] << '\n' << names[2] << '\n';
+        f << MAGIC << names[0] << '\n' << names[1] << '\n' << names[2] << '\n' << names[3] << '\n';
         f.write(cubin.data(), std::streamsize(cubin.size()));
         if (!f) return;
     }
@@ -263,7 +263,7 @@ std::vector<std::unique_ptr<JitEntry>> g_jit;
 
 // NVRTC build (or disk-cache hit) of the three kernels of (K, R, polys, W):
 // cubin + lowered names.  Needs no GPU.
-bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[3],
+bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[4],
                  std::string* cubin, std::string* err) {
     auto fail = [&](const std::string& m) {
         if (err) *err = m;
@@ -273,8 +273,9 @@ bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[3
     char cfg[160];
     std::snprintf(cfg, sizeof cfg, "pbvd::Cfg<pbvd::Code<%d, %d, %uu, %uu, %uu, %uu>, %d>", K, R,
                   polys[0], polys[1], R > 2 ? polys[2] : 0u, R > 3 ? polys[3] : 0u, W);
-    const std::string exprs[3] = {std::string("pbvd::fwd_kernel<") + cfg + ", false>",
+    const std::string exprs[4] = {std::string("pbvd::fwd_kernel<") + cfg + ", false>",
                                   std::string("pbvd::fwd_kernel<") + cfg + ", true>",
+                                  std::string("pbvd::fwd_kernel<") + cfg + ", true, true>",
                                   std::string("pbvd::tb_kernel<") + cfg + ">"};
     const std::string source = "// pbvd JIT: " + std::string(cfg) +
                                "\n#include \"fwd.cuh\"\n#include \"tb.cuh\"\n";
@@ -321,7 +322,7 @@ bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[3
         if (log.size() > 4000) log = log.substr(0, 4000) + "...";
         return fail(std::string("JIT: NVRTC compile failed: ") + n.errstr(r) + "\n" + log);
     }
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
         const char* low = nullptr;
         if (n.lowered(prog, exprs[i].c_str(), &low) != NVRTC_SUCCESS || !low) {
             n.destroy(&prog);
@@ -354,7 +355,7 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
         if (same) return &e->v;
     }
     auto ent = std::make_unique<JitEntry>();
-    std::string names[3];
+    std::string names[4];
     if (!jit_compile(K, R, polys, W, names, &ent->cubin, err)) return nullptr;
     cudaError_t e = cudaLibraryLoadData(&ent->lib, ent->cubin.data(), nullptr, nullptr, 0, nullptr,
                                         nullptr, 0);
@@ -362,8 +363,8 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
         cudaGetLastError();
         return fail(std::string("JIT: cudaLibraryLoadData: ") + cudaGetErrorString(e));
     }
-    cudaKernel_t ks[3] = {};
-    for (int i = 0; i < 3; ++i) {
+    cudaKernel_t ks[4] = {};
+    for (int i = 0; i < 4; ++i) {
         e = cudaLibraryGetKernel(&ks[i], ent->lib, names[i].c_str());
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -376,7 +377,8 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
     ent->v.jit = true;
     ent->v.k_fwd = reinterpret_cast<const void*>(ks[0]);
     ent->v.k_fused = reinterpret_cast<const void*>(ks[1]);
-    ent->v.k_tb = reinterpret_cast<const void*>(ks[2]);
+    ent->v.k_mirror = reinterpret_cast<const void*>(ks[2]);
+    ent->v.k_tb = reinterpret_cast<const void*>(ks[3]);
     ent->v.prepared = 0;
     g_jit.push_back(std::move(ent));
     return &g_jit.back()->v;
@@ -393,7 +395,7 @@ extern "C" int pbvd_jit_prebuild(int K, int R, const uint32_t* polys, int lanes,
     const int W = lanes == 0 ? pbvd::default_lanes(K) : lanes;
     pbvd::Variant shape{};
     std::string err;
-    std::string names[3], cubin;
+    std::string names[4], cubin;
     int rc = PBVD_OK;
     if (!pbvd::variant_shape(K, R, W, &shape)) {
         err = "no kernel shape for that (K, R, lanes)";

@@ -12,25 +12,26 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int MAX_EDGE = 32;      // edge blocks per launch (more -> extra launches)
 constexpr int MAX_MIRROR = 7;     // extra output destinations (peer GPUs' buffers)
 
-// Output destinations of the traceback: every 32-bit word / byte stored at
-// p[i] is also stored at p[i] + md[k] (bytes) for k < nm -- the other ranks'
-// gather buffers mapped into this process (CUDA IPC / peer access), so the
-// kernel's own stores perform the all-gather of the decoded bits.
-struct OutW {
-    uint32_t* p;
-    const int64_t* md;
-    int nm;
-    __device__ __forceinline__ void put(int64_t i, uint32_t v) const {
-        p[i] = v;
-        for (int k = 0; k < nm; ++k)
-            *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(p + i) + md[k]) = v;
+// Multi-GPU gather fused into the decode (pbvd_decode_blocks_mirrored): the
+// bytes [0, n) at src are copied to src + md[k] for k < nm -- the other
+// ranks' gather buffers mapped into this process (CUDA IPC / peer access),
+// by threads t = tid, tid + nthr, ... (32-bit words when aligned).
+__device__ __forceinline__ void mirror_copy(const uint8_t* src, int64_t n, const int64_t* md,
+                                            int nm, int tid, int nthr) {
+    if (((reinterpret_cast<uintptr_t>(src) | uintptr_t(n)) & 3) == 0) {
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+        for (int64_t i = tid; i < n / 4; i += nthr) {
+            const uint32_t v = s32[i];
+            for (int k = 0; k < nm; ++k)
+                *reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(src) + md[k] + 4 * i) = v;
+        }
+    } else {
+        for (int64_t i = tid; i < n; i += nthr) {
+            const uint8_t v = src[i];
+            for (int k = 0; k < nm; ++k) const_cast<uint8_t*>(src)[md[k] + i] = v;
+        }
     }
-    __device__ __forceinline__ void put8(int64_t i, uint8_t v) const {
-        uint8_t* b = reinterpret_cast<uint8_t*>(p);
-        b[i] = v;
-        for (int k = 0; k < nm; ++k) b[i + md[k]] = v;
-    }
-};
+}
 constexpr int S_HEAD = 8192;      // known-start sentinel, > v*128*R (reading c-12)
 
 // One "edge" block: a block whose forward span is not the uniform
@@ -75,7 +76,7 @@ struct FwdParams {
     int64_t out_bit0;      // bit offset of the first interior block in out
     int t0r, t1r;          // interior decoding range relative to lo (L, L+D)
     int word_out;          // 1: interior blocks store aligned 32-bit words
-    int n_mirror;          // extra output destinations (OutW)
+    int n_mirror;          // extra output destinations (fused mode, mirror_copy)
     int64_t mirror[MAX_MIRROR];   // byte offsets of the destinations from out
     unsigned long long* dbg;   // timing experiment only (PBVD_EXP_TIMING builds), else null
     EdgeDesc edges[MAX_EDGE];
@@ -92,8 +93,6 @@ struct TbParams {
     int word_out;          // 1: interior blocks store aligned 32-bit words
     int64_t out_bit0;      // bit offset of the first interior block in d_bits
     uint8_t* out;
-    int n_mirror;          // extra output destinations (OutW)
-    int64_t mirror[MAX_MIRROR];
     const uint32_t* dec_edge;
     const int32_t* start_edge;
     int span_edge_max;

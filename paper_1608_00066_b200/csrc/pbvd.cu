@@ -119,8 +119,10 @@ int ensure_prepared(pbvd_t h, const Variant* v) {
     std::lock_guard<std::mutex> lk(g_prep_mu);
     const uint64_t bit = uint64_t(1) << (h->device & 63);
     if (!(v->prepared & bit)) {
-        const std::pair<const void*, size_t> ks[3] = {
-            {v->k_fwd, v->smem_fwd}, {v->k_fused, v->smem_fused}, {v->k_tb, v->smem_tb}};
+        const std::pair<const void*, size_t> ks[4] = {{v->k_fwd, v->smem_fwd},
+                                                       {v->k_fused, v->smem_fused},
+                                                       {v->k_mirror, v->smem_fused},
+                                                       {v->k_tb, v->smem_tb}};
         for (const auto& k : ks) {
             cudaError_t e = cudaFuncSetAttribute(k.first, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  int(k.second));
@@ -294,7 +296,7 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     fp.start_edge = start_edge;
     fp.span_edge_max = span_edge_max;
     fp.out = out;
-    fp.n_mirror = h->n_mirror;
+    fp.n_mirror = h->fused ? h->n_mirror : 0;
     for (int k = 0; k < MAX_MIRROR; ++k) fp.mirror[k] = h->mirror[k];
     fp.t0r = int(L);
     fp.t1r = int(L + D);
@@ -307,8 +309,6 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     tp.t1r = int(L + D);
     tp.D = int(D);
     tp.out = out;
-    tp.n_mirror = h->n_mirror;
-    for (int k = 0; k < MAX_MIRROR; ++k) tp.mirror[k] = h->mirror[k];
     tp.dec_edge = dec_edge;
     tp.start_edge = start_edge;
     tp.span_edge_max = span_edge_max;
@@ -406,7 +406,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
             fp.dbg = dbg;
         }
 #endif
-        cudaError_t le = h->fused ? launch(v->k_fused, fgrid, v->NT, v->smem_fused, stream, fp, false)
+        cudaError_t le = h->fused ? launch(fp.n_mirror > 0 ? v->k_mirror : v->k_fused, fgrid, v->NT,
+                                           v->smem_fused, stream, fp, false)
                                   : launch(v->k_fwd, fgrid, v->NT, v->smem_fwd, stream, fp, false);
         if (le != cudaSuccess) return cuda_fail(h, le, "forward kernel launch");
 #ifdef PBVD_EXP_TIMING
@@ -439,6 +440,16 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
+    }
+    if (!h->fused && h->n_mirror > 0) {
+        // two-kernel mode: the mirrors get the call's output by copies after
+        // the traceback (fused mode copies inside the kernel, per warp)
+        const int64_t nbytes = (std::min<int64_t>(B1 * D, n_info) - B0 * D + 7) / 8;
+        for (int k = 0; k < h->n_mirror; ++k) {
+            cudaError_t e = cudaMemcpyAsync(out + h->mirror[k], out, size_t(nbytes), cudaMemcpyDefault,
+                                            stream);
+            if (e != cudaSuccess) return cuda_fail(h, e, "mirror copy");
+        }
     }
     return PBVD_OK;
 }

@@ -101,7 +101,7 @@ __device__ __forceinline__ void tb_step(TbState& t, const uint32_t* nrow, int wo
 // the same with a runtime phase (partial chunks)
 template <class CF>
 __device__ __forceinline__ void tb_step_rt(TbState& t, int ph, const uint32_t* nrow, int woff,
-                                           uint32_t hbit, const OutW& out32, int64_t word0,
+                                           uint32_t hbit, uint32_t* out32, int64_t word0,
                                            int nwords) {
     const uint32_t pb = 1u << ph;
     const uint32_t w0 = nrow[tb_word_index<CF>(t.q & ~pb, woff)];
@@ -109,7 +109,7 @@ __device__ __forceinline__ void tb_step_rt(TbState& t, int ph, const uint32_t* n
     const uint32_t dec = (t.wcur >> tb_bitpos<CF>(t.q, hbit)) & 1u;
     t.acc64 = (t.acc64 << 1) | dec;
     if ((t.e & 31) == 0 && t.e >= 0 && (t.e >> 5) < nwords)
-        out32.put(word0 + (t.e >> 5), uint32_t(t.acc64));
+        out32[word0 + (t.e >> 5)] = uint32_t(t.acc64);
     --t.e;
     t.q = (t.q & ~pb) | (dec << ph);
     t.wcur = dec ? w1 : w0;
@@ -130,12 +130,12 @@ __device__ __forceinline__ void tb_steps(TbState& t, const uint32_t*& row,
 template <class CF>
 __device__ __forceinline__ void tb_cycle(TbState& t, const uint32_t*& row,
                                          const uint32_t* last_below, int woff, uint32_t hbit,
-                                         const OutW& out32, int64_t word0, int nwords) {
+                                         uint32_t* out32, int64_t word0, int nwords) {
     tb_steps<CF, CF::V - 1>(t, row, last_below, woff, hbit);
     const int eb = t.e, ea = t.e - CF::V;          // steps had e = eb .. ea+1
     const int w = eb >> 5;                         // floor (eb >= 0 checked below)
     if (eb >= 0 && (w << 5) > ea && w < nwords)
-        out32.put(word0 + w, uint32_t(t.acc64 >> ((w << 5) - ea - 1)));
+        out32[word0 + w] = uint32_t(t.acc64 >> ((w << 5) - ea - 1));
     t.e = ea;
 }
 
@@ -199,7 +199,7 @@ __device__ __forceinline__ void tbc_load(RowT<CF> (&b)[CF::V], const uint32_t* r
 // v steps from row `row` (phase v-1) down, then the output word if complete
 template <class CF>
 __device__ __forceinline__ void tbc_cycle(TbState& t, const uint32_t* row, int woff, uint32_t sel,
-                                          uint32_t hbit, const OutW& out32, int64_t word0,
+                                          uint32_t hbit, uint32_t* out32, int64_t word0,
                                           int nwords) {
     RowT<CF> b[CF::V];
     tbc_load<CF, CF::V - 1>(b, row, woff, sel);
@@ -207,25 +207,25 @@ __device__ __forceinline__ void tbc_cycle(TbState& t, const uint32_t* row, int w
     const int eb = t.e, ea = t.e - CF::V;
     const int w = eb >> 5;
     if (eb >= 0 && (w << 5) > ea && w < nwords)
-        out32.put(word0 + w, uint32_t(t.acc64 >> ((w << 5) - ea - 1)));
+        out32[word0 + w] = uint32_t(t.acc64 >> ((w << 5) - ea - 1));
     t.e = ea;
 }
 template <class CF>
 __device__ __forceinline__ void tbc_step_rt(TbState& t, int ph, const uint32_t* row, int woff,
-                                            uint32_t sel, uint32_t hbit, const OutW& out32,
+                                            uint32_t sel, uint32_t hbit, uint32_t* out32,
                                             int64_t word0, int nwords) {
     const RowT<CF> b = row_bits<CF>(row, woff, sel);
     const uint32_t dec = row_bit<CF>(b, t.q, hbit);
     t.acc64 = (t.acc64 << 1) | dec;
     if ((t.e & 31) == 0 && t.e >= 0 && (t.e >> 5) < nwords)
-        out32.put(word0 + (t.e >> 5), uint32_t(t.acc64));
+        out32[word0 + (t.e >> 5)] = uint32_t(t.acc64);
     --t.e;
     t.q = (t.q & ~(1u << ph)) | (dec << ph);
 }
 // one chunk [lo, hi) of the compact walk; rows(r) = ring row of stage r
 template <class CF, int TT, class RowFn>
 __device__ __forceinline__ void tbc_chunk(TbState& t, int lo, int hi, int c, RowFn rows, int woff,
-                                          uint32_t sel, uint32_t hbit, const OutW& out32,
+                                          uint32_t sel, uint32_t hbit, uint32_t* out32,
                                           int64_t word0, int nwords) {
     constexpr int V = CF::V;
     if (hi - lo == TT && lo == c * TT) {
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
     // store aligned words; others (partial last block, unaligned output) bytes
     // (edge blocks too when their bits start on a word and fill whole words)
     const bool words = p.word_out && (!edge || (((out_bit0 | int64_t(t1r - t0r)) & 31) == 0));
-    const OutW out32{reinterpret_cast<uint32_t*>(p.out), p.mirror, p.n_mirror};
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(p.out);
     const int64_t word0 = out_bit0 >> 5;
     const int nwords = (nbits + 31) >> 5;
 
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
                     if (s < t1r) {
                         bacc = (bacc << 1) | ((q >> ph) & 1u);
                         const int eb = s - t0r;
-                        if ((eb & 7) == 0) out32.put8((out_bit0 + eb) >> 3, uint8_t(bacc & 0xffu));
+                        if ((eb & 7) == 0) p.out[(out_bit0 + eb) >> 3] = uint8_t(bacc & 0xffu);
                     }
                     q = (q & ~(1u << ph)) | (dec << ph);
                     ph = (ph == 0) ? V - 1 : ph - 1;
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
                 if (s < t1r) {
                     bacc = (bacc << 1) | ((q >> ph) & 1u);
                     const int eb = s - t0r;
-                    if ((eb & 7) == 0) out32.put8((out_bit0 + eb) >> 3, uint8_t(bacc & 0xffu));
+                    if ((eb & 7) == 0) p.out[(out_bit0 + eb) >> 3] = uint8_t(bacc & 0xffu);
                 }
                 ph = (ph == 0) ? V - 1 : ph - 1;
             }
@@ -490,8 +490,7 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
                                                int t0r, int t1r, int nblk,
                                                const uint32_t (&st)[TbwCfg<CF>::NBL],
                                                const int64_t (&obit)[TbwCfg<CF>::NBL], bool words,
-                                               uint8_t* out, const int64_t* mirror, int n_mirror,
-                                               int lane,
+                                               uint8_t* out, int lane,
                                                unsigned long long* dbg = nullptr) {
     using TC = TbwCfg<CF>;
     constexpr int V = CF::V, W = CF::W, WPS = CF::WPS, ROW = CF::ROW;
@@ -548,7 +547,7 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
     const int pe = span % V;
     const int nbits = t1r - t0r;
     const int nwords = (nbits + 31) >> 5;
-    const OutW out32{reinterpret_cast<uint32_t*>(out), mirror, n_mirror};
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
     TbState t[NBL];
     bool act[NBL];
     int woff[NBL];
@@ -591,7 +590,7 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
                     if (s < t1r) {
                         bacc[m] = (bacc[m] << 1) | ((q[m] >> ph) & 1u);
                         const int eb = s - t0r;
-                        if ((eb & 7) == 0) out32.put8((obit[m] + eb) >> 3, uint8_t(bacc[m] & 0xffu));
+                        if ((eb & 7) == 0) out[(obit[m] + eb) >> 3] = uint8_t(bacc[m] & 0xffu);
                     }
                     q[m] = (q[m] & ~(1u << ph)) | (dec << ph);
                     ph = (ph == 0) ? V - 1 : ph - 1;
@@ -609,7 +608,7 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
                 if (s < t1r) {
                     bacc[m] = (bacc[m] << 1) | ((q[m] >> ph) & 1u);
                     const int eb = s - t0r;
-                    if ((eb & 7) == 0) out32.put8((obit[m] + eb) >> 3, uint8_t(bacc[m] & 0xffu));
+                    if ((eb & 7) == 0) out[(obit[m] + eb) >> 3] = uint8_t(bacc[m] & 0xffu);
                 }
                 ph = (ph == 0) ? V - 1 : ph - 1;
             }
