@@ -347,6 +347,10 @@ def run_ours(args):
             fn, fargs = reduce_tensor(gbuf)
             all_args = [None] * world
             dist.all_gather_object(all_args, fargs)
+            for a in all_args:        # every rank's device must be reachable by peer access
+                pd = a[6] if isinstance(a[6], int) else local
+                if pd != local and not torch.cuda.can_device_access_peer(local, pd):
+                    raise RuntimeError(f"no peer access cuda:{local} -> cuda:{pd}")
             peer_bufs = [gbuf if r == rank else fn(*a) for r, a in enumerate(all_args)]
             o = sh.bit0 // 8
             mirrors = [peer_bufs[r].data_ptr() + o for r in range(world) if r != rank]
