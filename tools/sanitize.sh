@@ -8,3 +8,9 @@ for tool in memcheck racecheck synccheck initcheck; do
     echo "$tool [$args] rc=$rc $(echo "$out" | grep -E 'ERROR SUMMARY|bad bytes' | tr '\n' ' ')"
   done
 done
+# newer entry points (mirrored outputs, JIT codes, continuous stream, table depuncture, host pipeline)
+for tool in memcheck racecheck synccheck initcheck; do
+  out=$(timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python tools/debug_new_paths.py 2>&1)
+  rc=$?
+  echo "$tool [new paths] rc=$rc $(echo "$out" | grep -E 'ERROR SUMMARY|total bad' | tr '\n' ' ')"
+done
