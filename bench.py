@@ -234,9 +234,18 @@ def cpu_oracle_sample(code, punct, c, llr_host, n_info, target_s, ws0=0, b_first
              b0=b_first, nblk=nblk, window_stage0=ws0)
     dt = time.perf_counter() - t
     bits = min((b_first + nblk) * c["D"], n_info) - b_first * c["D"]
+    # and on one core (1 thread and all cores), a smaller sample
+    n1 = max(1, min(nblk, nblk // max(1, threads)))
+    t = time.perf_counter()
+    O.decode(code, llr_host, n_info, c["D"], c["L"], flags=flags, punct=punct, threads=1,
+             b0=b_first, nblk=n1, window_stage0=ws0)
+    dt1 = time.perf_counter() - t
+    bits1 = min((b_first + n1) * c["D"], n_info) - b_first * c["D"]
     return {"value": bits / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{nblk} of {nb} blocks ({bits} info bits) of the same stream, "
-                      f"{threads} pthreads, {dt:.2f} s wall"}
+                      f"{threads} pthreads, {dt:.2f} s wall",
+            "value_1_core": bits1 / dt1 / 1e9,
+            "sample_1_core": f"{n1} blocks, 1 thread, {dt1:.2f} s"}
 
 
 # ------------------------------------------------------------------ arms
