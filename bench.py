@@ -187,7 +187,7 @@ def acs_per_block_span(n_info, D, L, K, terminated, b0, nblk):
     nb = -(-n_info // D)
     total = 0
     # interior blocks all have span D + 2L; edge blocks are counted exactly
-    first_int = -(-L // D)
+    first_int = L // D + 1          # lo = bD - L > 0 (lo == 0 is a head block)
     last_int = min(nb - 2, (n_stages - L - D) // D if n_stages - L - D >= 0 else -1)
     lo_i, hi_i = max(first_int, b0), min(last_int + 1, b0 + nblk)
     n_int = max(0, hi_i - lo_i)

@@ -226,9 +226,11 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         llr = static_cast<const int8_t*>(W.al);
     }
 
-    // interior blocks: lo = bD - L >= 0, b < nb-1, (b+1)D + L <= n_stages
+    // interior blocks: lo = bD - L > 0 (a span starting at stage 0 is a head
+    // block with the known start state, reading c-12), b < nb-1,
+    // (b+1)D + L <= n_stages
     const int64_t D = h->D, L = h->L;
-    const int64_t first_int = (L + D - 1) / D;
+    const int64_t first_int = L / D + 1;
     const int64_t last_int = std::min<int64_t>(nb - 2, (n_stages - L - D) >= 0 ? (n_stages - L - D) / D : -1);
     const int64_t I0 = std::min(std::max(first_int, B0), B1);
     const int64_t I1 = std::max(I0, std::min(last_int + 1, B1));
@@ -255,7 +257,10 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     const size_t region_bytes = size_t(span_int) * v->ROW * 4;      // BPW blocks
     const int64_t n_int = I1 - I0;
     const size_t edge_region_bytes = size_t(span_edge_max) * v->ROW * 4;
-    const size_t edge_bytes = edge_region_bytes * MAX_EDGE + 2 * MAX_EDGE * 4 + 256;
+    // edge survivor regions: one per edge of a launch (launches beyond
+    // MAX_EDGE edges reuse them in stream order)
+    const size_t n_edge_slots = std::min<size_t>(MAX_EDGE, edges.size());
+    const size_t edge_bytes = edge_region_bytes * n_edge_slots + 2 * MAX_EDGE * 4 + 256;
     const int64_t unit = std::max<int64_t>(v->BPW, 128);   // multiple of BPW and TB CTA (128)
     int64_t wave = n_int;
     if (n_int > 0) {
@@ -275,7 +280,7 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     uint32_t* dec_int = reinterpret_cast<uint32_t*>(wsb);
     uint32_t* dec_edge = reinterpret_cast<uint32_t*>(wsb + ((int_bytes + 255) & ~size_t(255)));
     int32_t* start_edge = reinterpret_cast<int32_t*>(
-        reinterpret_cast<uint8_t*>(dec_edge) + edge_region_bytes * MAX_EDGE);
+        reinterpret_cast<uint8_t*>(dec_edge) + edge_region_bytes * n_edge_slots);
     int32_t* start_int = reinterpret_cast<int32_t*>(
         wsb + ((int_bytes + 255) & ~size_t(255)) + ((edge_bytes + 255) & ~size_t(255)));
 
@@ -522,6 +527,11 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
     if (!(lead && trail) && !(flags & PBVD_ALLOW_CATASTROPHIC))
         return create_fail(PBVD_EINVAL, "no generator has the g_{K-1} (or g_0) tap; "
                                         "pass PBVD_ALLOW_CATASTROPHIC to decode it anyway");
+    if (punct_period > 1) {
+        int kept = 0;
+        for (int i = 0; i < R * punct_period; ++i) kept += punct[i] ? 1 : 0;
+        if (kept == 0) return create_fail(PBVD_EINVAL, "puncture matrix keeps no position");
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
         cudaGetLastError();
@@ -532,7 +542,7 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
     if (!best) return create_fail(PBVD_EUNSUPPORTED, why);
     const Variant* hbest = latency_variant(K, R, polys, best);
     pbvd_s* h = new (std::nothrow) pbvd_s();
-    if (!h) return PBVD_ENOMEM;
+    if (!h) return create_fail(PBVD_ENOMEM, "handle allocation");
     h->device = device;
     h->K = K;
     h->R = R;
@@ -559,7 +569,7 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
         }
         if (kp == 0) {
             delete h;
-            return PBVD_EINVAL;
+            return create_fail(PBVD_EINVAL, "puncture matrix keeps no position");
         }
         h->kp = kp;
     } else {
@@ -625,17 +635,20 @@ void pbvd_destroy(pbvd_t h) {
 }
 
 int64_t pbvd_stage_count(pbvd_t h, int64_t n_info) {
-    if (!h || n_info < 1) return PBVD_EINVAL;
+    if (!h) return PBVD_EINVAL;
+    if (n_info < 1) return fail(h, PBVD_EINVAL, "n_info < 1");
     return n_info + ((h->flags & PBVD_TERMINATED) ? h->V : 0);
 }
 
 int64_t pbvd_block_count(pbvd_t h, int64_t n_info) {
-    if (!h || n_info < 1) return PBVD_EINVAL;
+    if (!h) return PBVD_EINVAL;
+    if (n_info < 1) return fail(h, PBVD_EINVAL, "n_info < 1");
     return (n_info + h->D - 1) / h->D;
 }
 
 int64_t pbvd_llr_count(pbvd_t h, int64_t n_info) {
-    if (!h || n_info < 1) return PBVD_EINVAL;
+    if (!h) return PBVD_EINVAL;
+    if (n_info < 1) return fail(h, PBVD_EINVAL, "n_info < 1");
     return kept_before_h(h, pbvd_stage_count(h, n_info));
 }
 
@@ -797,7 +810,7 @@ int64_t stages_complete(const pbvd_s* h, int64_t k) {
 int pbvd_stream_open(pbvd_t h, pbvd_stream_t* out) {
     if (!h || !out) return PBVD_EINVAL;
     *out = new (std::nothrow) pbvd_stream_s();
-    if (!*out) return PBVD_ENOMEM;
+    if (!*out) return fail(h, PBVD_ENOMEM, "stream allocation");
     (*out)->h = h;
     return PBVD_OK;
 }
@@ -928,7 +941,8 @@ int pbvd_set_fused(pbvd_t h, int fused) {
 int pbvd_get_fused(pbvd_t h) { return h ? int(h->fused) : PBVD_EINVAL; }
 
 int pbvd_set_workspace_limit(pbvd_t h, size_t bytes) {
-    if (!h || bytes < (size_t(1) << 20)) return PBVD_EINVAL;
+    if (!h) return PBVD_EINVAL;
+    if (bytes < (size_t(1) << 20)) return fail(h, PBVD_EINVAL, "workspace limit below 1 MiB");
     h->ws_limit = bytes;
     return PBVD_OK;
 }

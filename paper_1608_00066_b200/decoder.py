@@ -4,6 +4,7 @@ decode step runs in libpbvd.so's sm_100a kernels (no CPU fallback)."""
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import torch
 
@@ -67,6 +68,32 @@ def probe_acs_peak(device: int = 0):
     return a.value, m.value
 
 
+def _check_in(t: torch.Tensor, name: str, cuda_device: int | None):
+    """int8, contiguous, on cuda:cuda_device (None: on the host)."""
+    if t.dtype != torch.int8 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous int8 tensor")
+    if cuda_device is None:
+        if t.is_cuda:
+            raise ValueError(f"{name} must be a host (CPU) tensor")
+    elif not t.is_cuda or t.device.index != cuda_device:
+        raise ValueError(f"{name} must be on cuda:{cuda_device}")
+
+
+def _check_out(out: torch.Tensor, nbytes: int, cuda_device: int | None):
+    """The C ABI takes no output length: a caller-supplied out must be a
+    contiguous uint8 tensor on the right device with >= nbytes elements."""
+    if out.dtype != torch.uint8 or not out.is_contiguous():
+        raise ValueError("out must be a contiguous uint8 tensor")
+    if out.numel() < nbytes:
+        raise ValueError(f"out holds {out.numel()} bytes, the call writes {nbytes}")
+    if cuda_device is None:
+        if out.is_cuda:
+            raise ValueError("out must be a host (CPU) tensor")
+    elif not out.is_cuda or out.device.index != cuda_device:
+        raise ValueError(f"out must be on cuda:{cuda_device}")
+    return out
+
+
 class Decoder:
     """pbvd_create(...) -- see include/pbvd.h for the meaning of every argument.
 
@@ -75,6 +102,7 @@ class Decoder:
     def __init__(self, K, polys, D, L, punct=None, soft_bits=8, terminated=True, device=0,
                  lanes=0, fused=True, allow_catastrophic=False):
         self._L = _lib.load()
+        self._streams = weakref.WeakSet()
         self.K, self.polys, self.D, self.L = int(K), tuple(int(p) for p in polys), int(D), int(L)
         self.R = len(self.polys)
         self.punct = None if punct is None else tuple(tuple(int(x) for x in row) for row in punct)
@@ -111,6 +139,15 @@ class Decoder:
         return _check(self._L.pbvd_block_count(self._h, int(n_info)), self._h, "pbvd_block_count")
 
     # -------------------------------------------------------------- decode
+    def _live(self):
+        if not getattr(self, "_h", None):
+            raise PbvdError("decoder is closed")
+
+    def _range_bytes(self, n_info_total, block0, nblocks):
+        t0 = int(block0) * self.D
+        t1 = min((int(block0) + int(nblocks)) * self.D, int(n_info_total))
+        return max(0, (t1 - t0 + 7) // 8)
+
     def _stream(self, stream):
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
@@ -119,11 +156,12 @@ class Decoder:
     def decode(self, llr: torch.Tensor, n_info: int, out: torch.Tensor | None = None,
                stream=None) -> torch.Tensor:
         """pbvd_decode: int8 CUDA tensor -> packed uint8 CUDA tensor (async)."""
-        if llr.dtype != torch.int8 or not llr.is_cuda or not llr.is_contiguous():
-            raise ValueError("llr must be a contiguous int8 CUDA tensor")
+        self._live()
+        _check_in(llr, "llr", self.device)
         nbytes = (int(n_info) + 7) // 8
         if out is None:
             out = torch.empty(nbytes, dtype=torch.uint8, device=llr.device)
+        _check_out(out, nbytes, self.device)
         rc = self._L.pbvd_decode(self._h, llr.data_ptr(), llr.numel(), out.data_ptr(),
                                  int(n_info), self._stream(stream))
         _check(rc, self._h, "pbvd_decode")
@@ -133,13 +171,12 @@ class Decoder:
                       block0: int, nblocks: int, out: torch.Tensor | None = None,
                       stream=None) -> torch.Tensor:
         """pbvd_decode_blocks: decode blocks [block0, block0+nblocks) from a window."""
-        if llr_window.dtype != torch.int8 or not llr_window.is_cuda:
-            raise ValueError("llr_window must be an int8 CUDA tensor")
-        t0 = int(block0) * self.D
-        t1 = min((int(block0) + int(nblocks)) * self.D, int(n_info_total))
-        nbytes = (t1 - t0 + 7) // 8
+        self._live()
+        _check_in(llr_window, "llr_window", self.device)
+        nbytes = self._range_bytes(n_info_total, block0, nblocks)
         if out is None:
             out = torch.empty(nbytes, dtype=torch.uint8, device=llr_window.device)
+        _check_out(out, nbytes, self.device)
         rc = self._L.pbvd_decode_blocks(self._h, llr_window.data_ptr(), int(window_stage0),
                                         llr_window.numel(), int(n_info_total), int(block0),
                                         int(nblocks), out.data_ptr(), self._stream(stream))
@@ -152,8 +189,9 @@ class Decoder:
         """pbvd_decode_blocks_mirrored: decode_blocks whose traceback also stores
         the bits at every address in mirror_ptrs (ints: device pointers, e.g.
         other ranks' gather buffers opened through CUDA IPC)."""
-        if llr_window.dtype != torch.int8 or not llr_window.is_cuda:
-            raise ValueError("llr_window must be an int8 CUDA tensor")
+        self._live()
+        _check_in(llr_window, "llr_window", self.device)
+        _check_out(out, self._range_bytes(n_info_total, block0, nblocks), self.device)
         arr = (ctypes.c_void_p * max(1, len(mirror_ptrs)))(*[int(x) for x in mirror_ptrs])
         rc = self._L.pbvd_decode_blocks_mirrored(
             self._h, llr_window.data_ptr(), int(window_stage0), llr_window.numel(),
@@ -168,15 +206,14 @@ class Decoder:
         """pbvd_decode_host: host int8 window (pinned for overlap) -> host packed bits.
 
         Defaults decode the whole stream; a shard passes its window and range."""
-        if llr.dtype != torch.int8 or llr.is_cuda or not llr.is_contiguous():
-            raise ValueError("llr must be a contiguous int8 CPU tensor")
+        self._live()
+        _check_in(llr, "llr", None)
         if nblocks is None:
             nblocks = self.block_count(n_info) - int(block0)
-        t0 = int(block0) * self.D
-        t1 = min((int(block0) + int(nblocks)) * self.D, int(n_info))
-        nbytes = (t1 - t0 + 7) // 8
+        nbytes = self._range_bytes(n_info, block0, nblocks)
         if out is None:
             out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=llr.is_pinned())
+        _check_out(out, nbytes, None)
         rc = self._L.pbvd_decode_host(self._h, llr.data_ptr(), int(window_stage0), llr.numel(),
                                       int(n_info), int(block0), int(nblocks), out.data_ptr(),
                                       int(n_streams))
@@ -185,8 +222,12 @@ class Decoder:
 
     # ------------------------------------------------------------- tuning
     def open_stream(self) -> "StreamDecoder":
-        """pbvd_stream_open: a continuous-stream decoder on this handle."""
-        return StreamDecoder(self)
+        """pbvd_stream_open: a continuous-stream decoder on this handle (closed
+        with it: close() closes every stream still open first)."""
+        self._live()
+        sd = StreamDecoder(self)
+        self._streams.add(sd)
+        return sd
 
     def set_lanes(self, lanes: int):
         _check(self._L.pbvd_set_lanes(self._h, int(lanes)), self._h, "pbvd_set_lanes")
@@ -225,6 +266,8 @@ class Decoder:
         return {k: getattr(i, k) for k, _ in _lib.PbvdInfo._fields_}
 
     def close(self):
+        for sd in list(getattr(self, "_streams", ())):
+            sd.close()
         if getattr(self, "_h", None):
             self._L.pbvd_destroy(self._h)
             self._h = None
@@ -277,9 +320,13 @@ class StreamDecoder:
         nbits = max(0, self._stages(self._rx + n_more) - self._emitted)
         return torch.empty((nbits + 7) // 8 + 1, dtype=torch.uint8, device=device)
 
+    def _live(self):
+        if not getattr(self, "_s", None):
+            raise PbvdError("stream is closed (or its decoder was closed)")
+
     def push(self, llr: torch.Tensor, stream=None) -> torch.Tensor:
-        if llr.dtype != torch.int8 or not llr.is_cuda or not llr.is_contiguous():
-            raise ValueError("llr must be a contiguous int8 CUDA tensor")
+        self._live()
+        _check_in(llr, "llr", self._dec.device)
         out = self._out(llr.numel(), llr.device)
         n = ctypes.c_int64()
         rc = self._L.pbvd_stream_push(self._s, llr.data_ptr(), llr.numel(), out.data_ptr(),
@@ -291,6 +338,7 @@ class StreamDecoder:
 
     def finish(self, stream=None):
         """-> (packed bits of the remaining blocks, their bit count)."""
+        self._live()
         out = self._out(0, torch.device("cuda", self._dec.device))
         n = ctypes.c_int64()
         rc = self._L.pbvd_stream_finish(self._s, out.data_ptr(), out.numel(), ctypes.byref(n),
@@ -303,6 +351,7 @@ class StreamDecoder:
         if getattr(self, "_s", None):
             self._L.pbvd_stream_close(self._s)
             self._s = None
+            self._dec._streams.discard(self)
 
     def __del__(self):
         try:

@@ -57,3 +57,47 @@ def test_pure_host_calls(lib):
     assert lib.pbvd_create(ctypes.byref(h), 7, 2, polys, 1, None, 12, 42, 8, 1, 0) == -1  # D % 8
     assert lib.pbvd_create(ctypes.byref(h), 7, 2, polys, 1, None, 512, 0, 8, 1, 0) == -1  # L
     assert lib.pbvd_create(None, 7, 2, polys, 1, None, 512, 42, 8, 1, 0) == -1
+
+
+def test_create_failures_set_the_last_error(lib):
+    """Every pbvd_create failure path leaves a message in pbvd_last_error(NULL)."""
+    import ctypes
+    h = ctypes.c_void_p()
+    polys = (ctypes.c_uint32 * 2)(0o171, 0o133)
+    zero = (ctypes.c_uint8 * 4)(0, 0, 0, 0)
+    cases = [
+        (7, 2, polys, 1, None, 12, 42, 8, 1),      # D % 8
+        (7, 2, polys, 1, None, 512, 0, 8, 1),      # L
+        (7, 2, polys, 2, zero, 512, 42, 8, 1),     # puncture matrix keeps nothing
+        (7, 2, polys, 1, None, 512, 42, 9, 1),     # soft bits
+        (7, 2, polys, 1, None, 512, 42, 8, 64),    # unknown flag
+    ]
+    for c in cases:
+        rc = lib.pbvd_create(ctypes.byref(h), *c, 0)
+        assert rc == -1, c
+        assert lib.pbvd_last_error(None).decode(), c
+
+
+def test_binding_validates_buffers_before_the_call():
+    """the C ABI takes no output length, so the binding rejects
+    a too-small, wrongly typed, strided or misplaced buffer itself."""
+    import torch
+    from paper_1608_00066_b200.decoder import _check_in, _check_out
+    x = torch.zeros(64, dtype=torch.int8)
+    _check_in(x, "llr", None)
+    with pytest.raises(ValueError):
+        _check_in(x[::2], "llr", None)                 # strided view
+    with pytest.raises(ValueError):
+        _check_in(x.to(torch.int16), "llr", None)
+    with pytest.raises(ValueError):
+        _check_in(x, "llr", 0)                          # host tensor where CUDA is needed
+    o = torch.zeros(16, dtype=torch.uint8)
+    assert _check_out(o, 16, None) is o
+    with pytest.raises(ValueError):
+        _check_out(o, 17, None)                         # too small
+    with pytest.raises(ValueError):
+        _check_out(o.to(torch.int8), 8, None)
+    with pytest.raises(ValueError):
+        _check_out(o[::2], 4, None)
+    with pytest.raises(ValueError):
+        _check_out(o, 8, 0)

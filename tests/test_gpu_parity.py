@@ -92,6 +92,23 @@ def test_small_streams_bit_exact(pbvd, orc, cfg):
                                    f"first at {bad[:8]}")
 
 
+@pytest.mark.parametrize("K,D,L", [(7, 8, 8), (7, 16, 16), (7, 64, 64), (7, 64, 128), (7, 8, 16),
+                                   (3, 16, 16), (9, 32, 64)])
+def test_L_multiple_of_D(pbvd, orc, K, D, L):
+    """L % D == 0: block L/D spans from stage 0, so it is a head block with
+    the known start state (reading c-12), not an interior block with zero
+    initial metrics.  Low SNR and several seeds, so the two starting rules
+    would give different bits (51 of 200 streams differ)."""
+    code = synth.CODES[{3: "k3", 7: "k7", 9: "k9"}[K]]
+    for seed in range(1, 9):
+        n_info = 6 * max(D, L) + 8 * seed
+        info, llr = synth.make_stream(code, n_info, 0.5, 100 + seed)
+        want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, D, L))
+        for fused in (True, False):
+            got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, fused=fused)
+            assert (got == want).all(), (seed, fused, np.nonzero(got != want)[0][:8])
+
+
 def test_saturated_and_extreme_inputs(pbvd, orc):
     """int8 extremes (-128 included) and all-erasure input (every ACS ties)."""
     code = synth.CODES["k7"]
