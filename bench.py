@@ -96,10 +96,13 @@ def describe(c, code, n_total, world):
 
 
 class ClockSampler:
-    """Samples SM clock and throttle reasons through NVML while running."""
+    """Samples SM clock and throttle reasons through NVML (every `period` s)
+    while running; mark() brackets the timed region, whose samples are also
+    summarised on their own."""
 
-    def __init__(self, device_index, period=0.005):
+    def __init__(self, device_index, period=0.001):
         self.period, self.samples, self.reasons = period, [], set()
+        self.marks = []
         self.max_mhz = None
         self._stop = threading.Event()
         try:
@@ -130,6 +133,9 @@ class ClockSampler:
                 pass
             time.sleep(self.period)
 
+    def mark(self):
+        self.marks.append(len(self.samples))
+
     def __enter__(self):
         if self.nv is not None:
             self.t = threading.Thread(target=self._run, daemon=True)
@@ -145,8 +151,13 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                     "samples": 0}
+        timed = self.samples[self.marks[0]:self.marks[1]] if len(self.marks) >= 2 else []
         return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "period_ms": self.period * 1e3,
+                "window": "warm-up + timed steps + profiled pass",
+                "timed_sm_mhz": float(statistics.median(timed)) if timed else None,
+                "timed_samples": len(timed)}
 
 
 # ---- ACS roofline derived from unit counts and clocks ----
@@ -201,13 +212,17 @@ def acs_per_block_span(n_info, D, L, K, terminated, b0, nblk):
     return total
 
 
-def load_traffic():
-    """dram bytes per forward launch from the committed ncu summary, if any."""
+def load_traffic(workload, fused):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/latest_fwd_ncu.json), if it was captured on this
+    workload and kernel mode; else None."""
     p = ROOT / "profiles" / "latest_fwd_ncu.json"
     if p.exists():
         try:
             d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_launch"), d
+            ent = d.get("captures", {}).get(f"{workload}:{'fused' if fused else 'two'}")
+            if ent:
+                return ent.get("dram_bytes_per_launch"), ent
         except Exception:
             pass
     return None, None
@@ -246,6 +261,46 @@ def cpu_oracle_sample(code, punct, c, llr_host, n_info, target_s, ws0=0, b_first
                       f"{threads} pthreads, {dt:.2f} s wall",
             "value_1_core": bits1 / dt1 / 1e9,
             "sample_1_core": f"{n1} blocks, 1 thread, {dt1:.2f} s"}
+
+
+def bench_parity(code, punct, c, n_total, world, got, dev):
+    """Oracle parity of a decoded stream `got` (packed, the whole n_total
+    bits): every block up to 2^28 bits, else sampled runs in every rank's
+    block range (see run_ours)."""
+    from oracle import oracle as O
+    from paper_1608_00066_b200 import shard as S
+    O.build()
+    D, L, K = c["D"], c["L"], code["K"]
+    R = len(code["polys"])
+    nb = -(-n_total // D)
+    n_stages = n_total + K - 1
+    runs = []
+    if n_total <= (1 << 28):
+        runs = [(b0, min(1 << 18, nb - b0)) for b0 in range(0, nb, 1 << 18)]
+    else:
+        rng = np.random.default_rng(12345)
+        for r in range(world):
+            sh = S.plan(n_total, D, L, K, True, world, r)
+            b0, b1 = sh.block0, sh.block0 + sh.nblocks
+            mid = int(rng.integers(b0, max(b0 + 1, b1 - 64)))
+            runs += [(b0, min(64, b1 - b0)), (max(b0, b1 - 64), min(64, b1 - b0)),
+                     (mid, min(64, b1 - mid))]
+    checked, ok = 0, True
+    for b0, nblk in runs:
+        lo = max(0, b0 * D - L)
+        hi = n_stages if b0 + nblk == nb else min(n_stages, (b0 + nblk) * D + L)
+        win = synth.make_window(code, n_total, c["ebn0"], c["seed"], lo, hi, punct, c["hard"],
+                                device=dev).cpu().numpy()
+        want = O.pack_bits(O.decode(code, win, n_total, D, L, punct=punct, b0=b0, nblk=nblk,
+                                    window_stage0=lo))
+        t0 = b0 * D
+        seg = got[t0 // 8:t0 // 8 + want.size]
+        ok &= bool(np.array_equal(seg, want))
+        checked += nblk
+    return {"blocks_checked": checked, "blocks_total": nb, "bit_exact": ok,
+            "scope": ("every block" if checked == nb else
+                      f"first/last/random 64-block runs of each of the {world} ranks' ranges") +
+                     (" of the gathered stream" if world > 1 else "")}
 
 
 # ------------------------------------------------------------------ arms
@@ -341,53 +396,58 @@ def run_ours(args):
 
     # N > 1: the gather of the decoded bits (a10).  Default: fused into
     # the traceback -- every rank's gather buffer is mapped into every other
-    # rank through CUDA IPC (peer access over NVLink) and the decode kernel
-    # stores each output word to all of them (pbvd_decode_blocks_mirrored);
-    # checked against an NCCL all_gather after the warm-up, with the NCCL
-    # all_gather as the fallback (PBVD_BENCH_GATHER=nccl forces it).
+    # rank through CUDA IPC (pbvd_ipc_export / pbvd_ipc_open: peer access
+    # over NVLink) and the decode kernel stores each output word to all of
+    # them (pbvd_decode_blocks_mirrored); checked against an NCCL all_gather
+    # after the warm-up, with the NCCL all_gather as the fallback
+    # (PBVD_BENCH_GATHER=nccl forces it; config.gather says which ran and why).
     gather_mode = "none" if world == 1 else os.environ.get("PBVD_BENCH_GATHER", "peer")
-    gbuf, mirrors = None, []
+    gather_note = ""
+    gbuf, mirrors, peer = None, [], None
     if gather_mode == "peer":
-        ok = 1
         try:
-            from torch.multiprocessing.reductions import reduce_tensor
-            total_bytes = (n_total + 7) // 8
-            gbuf = torch.zeros(total_bytes, dtype=torch.uint8, device=dev)
-            fn, fargs = reduce_tensor(gbuf)
-            all_args = [None] * world
-            dist.all_gather_object(all_args, fargs)
-            for a in all_args:        # every rank's device must be reachable by peer access
-                pd = a[6] if isinstance(a[6], int) else local
-                if pd != local and not torch.cuda.can_device_access_peer(local, pd):
-                    raise RuntimeError(f"no peer access cuda:{local} -> cuda:{pd}")
-            peer_bufs = [gbuf if r == rank else fn(*a) for r, a in enumerate(all_args)]
-            o = sh.bit0 // 8
-            mirrors = [peer_bufs[r].data_ptr() + o for r in range(world) if r != rank]
-            out = gbuf[o:o + sh.nbytes]
+            gbuf = torch.zeros((n_total + 7) // 8, dtype=torch.uint8, device=dev)
+            peer = S.PeerGather(gbuf)
+            mirrors = peer.mirrors(sh)
+            out = gbuf[sh.bit0 // 8:sh.bit0 // 8 + sh.nbytes]
         except Exception as ex:  # pragma: no cover - depends on the box
-            print(f"peer gather setup failed ({ex}); NCCL all_gather instead", file=sys.stderr)
-            ok = 0
-        flag = torch.tensor([ok], dtype=torch.int32, device=cdev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if not int(flag.item()):
-            gather_mode = "nccl"
+            gather_note = f"peer gather setup failed ({ex})"
+            print(gather_note + "; NCCL all_gather instead", file=sys.stderr)
+            gather_mode, peer, gbuf = "nccl", None, None
             out = torch.empty(sh.nbytes, dtype=torch.uint8, device=dev)
+    elif gather_mode == "nccl":
+        gather_note = "forced by PBVD_BENCH_GATHER=nccl"
+    done_flag = torch.zeros(1, dtype=torch.int32, device=cdev)
 
-    def step():
+    def decode_part():
         if gather_mode == "peer":
             dec.decode_blocks_mirrored(llr, sh.stage0, n_total, sh.block0, sh.nblocks, out,
                                        mirrors)
+        else:
+            dec.decode_blocks(llr, sh.stage0, n_total, sh.block0, sh.nblocks, out=out)
+
+    def gather_part():
+        if gather_mode == "peer":
+            # every rank's stores into this buffer are complete once every
+            # rank's decode kernel has retired: a one-word all_reduce queued
+            # behind the decode on each rank's stream
+            dist.all_reduce(done_flag)
             return gbuf
-        dec.decode_blocks(llr, sh.stage0, n_total, sh.block0, sh.nblocks, out=out)
         if world > 1:
             return S.gather_bits(out.to(cdev), sh, n_total, D)
         return out
+
+    def step():
+        decode_part()
+        return gather_part()
 
     # measured throughput of the all-ALU ACS sequence (pbvd_probe_acs_peak):
     # reported beside the derived roofline as a cross-check
     probe_acs, _ = P.probe_acs_peak(local)
     probe_bal, _ = P.probe_acs_balanced(local)
 
+    clk = ClockSampler(local, period=0.001)
+    clk.__enter__()               # sampled from the warm-up through the profiled pass
     for _ in range(args.warmup):
         flush.zero_()
         gathered = step()
@@ -402,29 +462,41 @@ def run_ours(args):
         good = torch.tensor([int(torch.equal(ref.to(dev), gbuf))], dtype=torch.int32, device=cdev)
         dist.all_reduce(good, op=dist.ReduceOp.MIN)
         if not int(good.item()):
-            print("peer gather check failed; NCCL all_gather instead", file=sys.stderr)
+            gather_note = "peer gather check against an NCCL all_gather failed"
+            print(gather_note + "; NCCL all_gather instead", file=sys.stderr)
             gather_mode = "nccl"
             out = out.clone()
         torch.cuda.synchronize()
         dist.barrier()
 
     stream = torch.cuda.current_stream(dev)
-    times, launches = [], 0
+    times, dec_times, gat_times, launches = [], [], [], 0
     dec.set_profiling(False)          # no events inside a decode: the timed region is pure
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            gathered = step()
-            e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
-            launches += dec.kernel_times()[2]
-        torch.cuda.synchronize()
+    clk.mark()
+    for _ in range(args.steps):
         if world > 1:
-            dist.barrier()
+            dist.barrier()            # every rank starts the step together
+            torch.cuda.synchronize()
+        # L2 flush; the host enqueues the decode while the memset runs, so
+        # the timed region holds no host launch latency
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        em = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        decode_part()
+        em.record(stream)
+        gathered = gather_part()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        dec_times.append(e0.elapsed_time(em))
+        gat_times.append(em.elapsed_time(e1))
+        launches += dec.kernel_times()[2]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk.mark()
     # per-kernel times (CUDA events around each launch on the decode stream),
     # a separate pass of the same steps -- the events break the PDL overlap of
     # the two kernels, so they are kept out of the timed region above
@@ -432,16 +504,18 @@ def run_ours(args):
     fwd, tb = [], []
     for _ in range(max(10, min(args.steps, 50))):
         flush.zero_()
-        step()
+        decode_part()
         torch.cuda.synchronize()
         f, t, n = dec.kernel_times()
         fwd.append(f)
         tb.append(t)
-    total_ms = sum(times)
-    tms = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
+    clk.__exit__()
+    # max over ranks: of the step total, and of the decode / gather parts
+    tms = torch.tensor([sum(times), sum(dec_times), sum(gat_times)], dtype=torch.float64,
+                       device=cdev)
     if world > 1:
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
-    total_ms = float(tms.item())
+    total_ms, dec_ms_tot, gat_ms_tot = (float(x) for x in tms.tolist())
     ms_per_step = total_ms / args.steps
     value = n_total / (ms_per_step * 1e-3) / 1e9
 
@@ -464,12 +538,18 @@ def run_ours(args):
     nb_rank = sh.nblocks
     dec_bytes = nb_rank * span * N // 8
     dec_read = nb_rank * (span - L - (K - 1)) * N // 8
-    alg_bytes = in_bytes + dec_bytes + (dec_read if dec.fused else 0)
+    out_bytes = sh.nbytes
+    # the algorithmic HBM bytes of the fused single-kernel
+    # design are the soft input (halo re-reads included) and the packed
+    # output -- the survivors never need to leave the chip (~2.5 B/bit for
+    # C2); the two-kernel design adds the survivor write and read-back
+    # (20.4 B/bit).  `traffic` (ncu) shows what the kernel really moves.
+    alg_bytes = in_bytes + out_bytes + (0 if dec.fused else dec_bytes + dec_read)
     fwd_hbm_gbs = alg_bytes / (fwd_ms * 1e-3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    traffic, _ = load_traffic()
+    traffic, _ = load_traffic(args.workload, dec.fused)
     kname = "fwd_kernel<fused>" if dec.fused else "fwd_kernel"
     roofline = {
         "bound": "alu", "achieved": achieved / 1e12, "peak": peak_acs / 1e12, "unit": "Tacs/s",
@@ -484,37 +564,38 @@ def run_ours(args):
         "probe_balanced_tacs": probe_bal / 1e12,
         "acs_per_launch": acs_step, "kernel_ms": fwd_ms, "tb_kernel_ms": tb_ms,
         "kernel_share_of_step": fwd_ms / ms_per_step,
-        "hbm": {"algorithmic_bytes_per_launch": alg_bytes, "achieved_gbs": fwd_hbm_gbs,
+        "hbm": {"algorithmic_bytes_per_launch": alg_bytes,
+                "algorithmic_bytes_per_bit": alg_bytes / max(1, sh.bit1 - sh.bit0),
+                "two_kernel_design_bytes_per_launch": in_bytes + out_bytes + dec_bytes + dec_read,
+                "dram_bytes_per_launch_ncu": traffic,
+                "dram_bytes_per_bit_ncu": (traffic / max(1, sh.bit1 - sh.bit0)) if traffic else None,
+                "achieved_gbs": fwd_hbm_gbs,
                 "peak_gbs": hbm_peak, "frac": fwd_hbm_gbs / hbm_peak,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
     }
 
-    # ---- parity spot check inside the bench (never timed) ------------------
+    # ---- parity inside the bench (never timed) -----------------------------
+    # rank 0 checks the GATHERED stream (every rank's blocks, N > 1) or its
+    # own output (N = 1) against the oracle: every block when the stream has
+    # <= 2^28 bits (C2 at N <= 8: a few s on the host cores), else, for each
+    # rank's range, its first, last and a seeded random run of 64 blocks,
+    # each run's soft window regenerated here from the same seeds
     parity = None
     if rank == 0:
         try:
-            from oracle import oracle as O
-            O.build()
-            nchk = min(sh.nblocks, 64)
-            # first blocks of the rank plus the last ones (edges)
-            blocks = list(range(sh.block0, sh.block0 + nchk // 2)) + \
-                list(range(sh.block0 + sh.nblocks - nchk // 2, sh.block0 + sh.nblocks))
-            llr_h = llr.cpu().numpy()
-            got = np.unpackbits(out.cpu().numpy(), bitorder="little")
-            ok = True
-            for b in sorted(set(blocks)):
-                want = O.decode(code, llr_h, n_total, D, L, punct=punct, b0=b, nblk=1,
-                                window_stage0=sh.stage0, threads=1)
-                t0 = (b - sh.block0) * D
-                ok &= bool((got[t0:t0 + want.size] == want).all())
-            parity = {"blocks_checked": len(set(blocks)), "bit_exact": ok}
+            parity = bench_parity(code, punct, c, n_total, world,
+                                  (gathered if world > 1 else out).cpu().numpy(), dev)
         except Exception as e:  # pragma: no cover
             parity = {"error": str(e)}
+    if world > 1:
+        dist.barrier()
 
     # ---- end to end through the C ABI with host buffers ---------------------
     e2e = None
+    llr_h = None
     if not args.no_e2e:
-        llr_h = llr.cpu().pin_memory()
+        llr_h = torch.empty(llr.shape, dtype=llr.dtype, pin_memory=True)   # one host copy
+        llr_h.copy_(llr)
         out_h = torch.empty(sh.nbytes, dtype=torch.uint8).pin_memory()
         # warm-up (untimed): host-lane streams and staging buffers, and the
         # host/PCIe path itself -- freshly pinned buffers copy at ~60 % of the
@@ -572,7 +653,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         O.build()
-        cpu = cpu_oracle_sample(code, punct, c, llr.cpu().numpy(), n_total, args.cpu_seconds,
+        host = llr_h if llr_h is not None else llr.cpu()
+        cpu = cpu_oracle_sample(code, punct, c, host.numpy(), n_total, args.cpu_seconds,
                                 ws0=sh.stage0, b_first=sh.block0, max_blocks=sh.nblocks)
 
     if world > 1:
@@ -589,13 +671,25 @@ def run_ours(args):
                        "parallelism": f"block-range shards x{world}",
                        "gather": {"none": "none (1 GPU)",
                                   "peer": "fused into the traceback: stores to every rank's "
-                                          "buffer over CUDA IPC / NVLink",
-                                  "nccl": "NCCL all_gather"}[gather_mode]},
+                                          "buffer over CUDA IPC / NVLink (completion: one "
+                                          "all_reduce word behind the decode)",
+                                  "nccl": "NCCL all_gather"}[gather_mode] +
+                                 (f" [{gather_note}]" if gather_note else ""),
+                       "step_barrier": "dist.barrier + synchronize before every timed step"
+                                       if world > 1 else "none (1 GPU)"},
+            "t_G": {"decode_ms": dec_ms_tot / args.steps, "gather_ms": gat_ms_tot / args.steps,
+                    "note": "per step, each the max over ranks of its CUDA-event time on the "
+                            "decode stream (SURVEY §8(d): max-rank decode + gather)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()            # no rank still reads or writes a peer buffer
+        if peer is not None:
+            peer.close()
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

@@ -70,6 +70,13 @@ enum pbvd_status {
 #define PBVD_TERMINATED (1u << 0) /* stream ends with K-1 zero tail stages (c-13) */
 #define PBVD_ALLOW_CATASTROPHIC (1u << 1) /* accept generators with no g_{K-1} or no g_0
                                             tap (SPEC S:53-55 warning-class override) */
+#define PBVD_START_ZERO (1u << 2) /* the paper's own traceback start (§III.A: "a
+                                    traceback procedure starts from a random state (state
+                                    S_0, for example)"; Alg. 1 K2 initialises state = 0,
+                                    P:215): EVERY block, interior, head and last, traces
+                                    back from state 0 instead of the min-PM state of P:75
+                                    (the alternative of reading c-10).  Costs BER at short
+                                    L (Fig. 4; DESIGN.md §10 NEXT 3). */
 
 /* Create a decoder on CUDA device `device`.
  *   K          constraint length, 3..12 (2^(K-1) states)
@@ -85,7 +92,7 @@ enum pbvd_status {
  *              whole output bytes)
  *   L          truncation / traceback length (M = L), 1 <= L
  *   soft_bits  quantisation of the input, 1..8 (1 = hard +-1); advisory only
- *   flags      PBVD_TERMINATED | PBVD_ALLOW_CATASTROPHIC, or 0
+ *   flags      PBVD_TERMINATED | PBVD_ALLOW_CATASTROPHIC | PBVD_START_ZERO, or 0
  * Kernels: the codes listed by pbvd_supported() are compiled into the
  * library; any other (K, R, polys) is compiled at create time from the same
  * kernel templates with NVRTC (libnvrtc.so.12 loaded on demand; a few seconds
@@ -266,6 +273,30 @@ int pbvd_jit_prebuild(int K, int R, const uint32_t *polys, int lanes, char *msg,
 /* Message of the last failure on h; for h == NULL, of the calling thread's
  * last failed pbvd_create. */
 const char *pbvd_last_error(pbvd_t h);
+
+/* Gather buffers shared across processes (the multi-GPU "decoded bits are
+ * gathered" step, §III.A, fused into the decode by
+ * pbvd_decode_blocks_mirrored): plumbing over CUDA IPC, so that every rank can
+ * map every other rank's gather buffer and the traceback can store into it
+ * over NVLink / NVSwitch.
+ *   pbvd_ipc_export  d_ptr: any device pointer inside a cudaMalloc'ed
+ *                    allocation of this process (e.g. a torch tensor's
+ *                    data_ptr).  Writes the allocation's IPC handle
+ *                    (PBVD_IPC_HANDLE_BYTES bytes, caller-owned) and d_ptr's
+ *                    byte offset from the allocation base.
+ *   pbvd_ipc_open    maps (handle, offset) of ANOTHER process into this one on
+ *                    `device` (peer access enabled lazily) and returns the
+ *                    pointer matching the exporter's d_ptr.  The mapping stays
+ *                    valid until pbvd_ipc_close; the exporter must keep its
+ *                    allocation alive until every importer has closed it.
+ *   pbvd_ipc_close   unmaps a pointer from pbvd_ipc_open (same offset/device).
+ * Errors: PBVD_EINVAL (null / not a device allocation), PBVD_ECUDA (the CUDA
+ * IPC call failed -- e.g. no peer access between the devices); the message is
+ * in pbvd_last_error(NULL).  Synchronous. */
+#define PBVD_IPC_HANDLE_BYTES 64
+int pbvd_ipc_export(const void *d_ptr, void *handle, int64_t *offset);
+int pbvd_ipc_open(const void *handle, int64_t offset, int device, void **d_ptr);
+int pbvd_ipc_close(void *d_ptr, int64_t offset, int device);
 
 #ifdef __cplusplus
 }

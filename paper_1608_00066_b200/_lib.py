@@ -12,6 +12,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libpbvd.so"
 PBVD_OK = 0
 PBVD_TERMINATED = 1
 PBVD_ALLOW_CATASTROPHIC = 2
+PBVD_START_ZERO = 4
 
 EXPORTS = (
     "pbvd_create", "pbvd_destroy", "pbvd_llr_count", "pbvd_stage_count", "pbvd_block_count",
@@ -21,8 +22,9 @@ EXPORTS = (
     "pbvd_supported", "pbvd_strerror", "pbvd_last_error", "pbvd_probe_acs_peak",
     "pbvd_probe_acs_balanced", "pbvd_jit_prebuild",
     "pbvd_stream_open", "pbvd_stream_push", "pbvd_stream_finish", "pbvd_stream_close",
-    "pbvd_decode_blocks_mirrored",
+    "pbvd_decode_blocks_mirrored", "pbvd_ipc_export", "pbvd_ipc_open", "pbvd_ipc_close",
 )
+PBVD_IPC_HANDLE_BYTES = 64
 
 
 class PbvdInfo(ctypes.Structure):
@@ -106,5 +108,11 @@ def load(path: os.PathLike | None = None):
     L.pbvd_strerror.restype = cp
     L.pbvd_last_error.argtypes = [h]
     L.pbvd_last_error.restype = cp
+    L.pbvd_ipc_export.argtypes = [vp, vp, ctypes.POINTER(i64)]
+    L.pbvd_ipc_export.restype = i32
+    L.pbvd_ipc_open.argtypes = [vp, i64, i32, ctypes.POINTER(vp)]
+    L.pbvd_ipc_open.restype = i32
+    L.pbvd_ipc_close.argtypes = [vp, i64, i32]
+    L.pbvd_ipc_close.restype = i32
     _lib = L
     return L

@@ -903,6 +903,9 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         kA = min(kA, __shfl_xor_sync(0xffffffffu, kA, o));
         kB = min(kB, __shfl_xor_sync(0xffffffffu, kB, o));
     }
+    // the paper's own rule (Alg. 1 K2 "state = 0"): no state
+    // estimation, every block traces back from state S_0
+    if (p.start_zero) kA = kB = 0u;
     if constexpr (FUSED) {
         // traceback of this warp's blocks, lane i = block i (+32, +64 ...)
         constexpr int NBL = TbwCfg<CF>::NBL;

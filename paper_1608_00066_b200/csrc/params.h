@@ -76,6 +76,7 @@ struct FwdParams {
     int64_t out_bit0;      // bit offset of the first interior block in out
     int t0r, t1r;          // interior decoding range relative to lo (L, L+D)
     int word_out;          // 1: interior blocks store aligned 32-bit words
+    int start_zero;        // 1: every traceback starts in state 0 (PBVD_START_ZERO)
     int n_mirror;          // extra output destinations (fused mode, mirror_copy)
     int64_t mirror[MAX_MIRROR];   // byte offsets of the destinations from out
     unsigned long long* dbg;   // timing experiment only (PBVD_EXP_TIMING builds), else null

@@ -305,6 +305,7 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     for (int k = 0; k < MAX_MIRROR; ++k) fp.mirror[k] = h->mirror[k];
     fp.t0r = int(L);
     fp.t1r = int(L + D);
+    fp.start_zero = (h->flags & PBVD_START_ZERO) ? 1 : 0;
 
     TbParams tp{};
     tp.dec = dec_int;
@@ -513,7 +514,7 @@ int pbvd_create(pbvd_t* out, int K, int R, const uint32_t* polys, int punct_peri
     if (D < 8 || (D % 8) != 0 || L < 1 || D > (1 << 24) || L > (1 << 20))
         return create_fail(PBVD_EINVAL, "need D >= 8, D % 8 == 0, L >= 1");
     if (soft_bits < 1 || soft_bits > 8) return create_fail(PBVD_EINVAL, "soft_bits outside 1..8");
-    if (flags & ~(PBVD_TERMINATED | PBVD_ALLOW_CATASTROPHIC))
+    if (flags & ~(PBVD_TERMINATED | PBVD_ALLOW_CATASTROPHIC | PBVD_START_ZERO))
         return create_fail(PBVD_EINVAL, "unknown flag");
     uint32_t lead = 0, trail = 0;
     for (int r = 0; r < R; ++r) {
@@ -1025,5 +1026,69 @@ const char* pbvd_strerror(int code) {
 }
 
 const char* pbvd_last_error(pbvd_t h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+// ---- gather buffers across processes (CUDA IPC; the fused gather of P:112)
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (the library
+// links cudart statically and not libcuda)
+typedef int (*AddrRangeFn)(uintptr_t*, size_t*, uintptr_t);
+AddrRangeFn addr_range_fn() {
+    static AddrRangeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return AddrRangeFn(nullptr);
+        return reinterpret_cast<AddrRangeFn>(f);
+    }();
+    return fn;
+}
+}  // namespace
+
+int pbvd_ipc_export(const void* d_ptr, void* handle, int64_t* offset) {
+    if (!d_ptr || !handle || !offset) return create_fail(PBVD_EINVAL, "null argument");
+    AddrRangeFn fn = addr_range_fn();
+    if (!fn) return create_fail(PBVD_ECUDA, "cuMemGetAddressRange unavailable");
+    uintptr_t base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<uintptr_t>(d_ptr)) != 0)
+        return create_fail(PBVD_EINVAL, "not a device allocation");
+    cudaIpcMemHandle_t hd;
+    cudaError_t e = cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return create_fail(PBVD_ECUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    }
+    static_assert(sizeof(hd) == PBVD_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &hd, sizeof(hd));
+    *offset = int64_t(reinterpret_cast<uintptr_t>(d_ptr) - base);
+    return PBVD_OK;
+}
+
+int pbvd_ipc_open(const void* handle, int64_t offset, int device, void** d_ptr) {
+    if (!handle || !d_ptr || offset < 0) return create_fail(PBVD_EINVAL, "null argument");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return create_fail(PBVD_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    *d_ptr = static_cast<uint8_t*>(base) + offset;
+    return PBVD_OK;
+}
+
+int pbvd_ipc_close(void* d_ptr, int64_t offset, int device) {
+    if (!d_ptr || offset < 0) return create_fail(PBVD_EINVAL, "null argument");
+    DeviceGuard g(device);
+    cudaError_t e = cudaIpcCloseMemHandle(static_cast<uint8_t*>(d_ptr) - offset);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return create_fail(PBVD_ECUDA, std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e));
+    }
+    return PBVD_OK;
+}
 
 }  // extern "C"

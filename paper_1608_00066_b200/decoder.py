@@ -100,13 +100,14 @@ class Decoder:
     punct: None or an R x P keep matrix (rows in generator order)."""
 
     def __init__(self, K, polys, D, L, punct=None, soft_bits=8, terminated=True, device=0,
-                 lanes=0, fused=True, allow_catastrophic=False):
+                 lanes=0, fused=True, allow_catastrophic=False, start_zero=False):
         self._L = _lib.load()
         self._streams = weakref.WeakSet()
         self.K, self.polys, self.D, self.L = int(K), tuple(int(p) for p in polys), int(D), int(L)
         self.R = len(self.polys)
         self.punct = None if punct is None else tuple(tuple(int(x) for x in row) for row in punct)
         self.terminated = bool(terminated)
+        self.start_zero = bool(start_zero)
         self.device = int(device)
         arr = (ctypes.c_uint32 * self.R)(*self.polys)
         if self.punct is None:
@@ -119,7 +120,8 @@ class Decoder:
         rc = self._L.pbvd_create(ctypes.byref(h), self.K, self.R, arr, P, pp, self.D, self.L,
                                  int(soft_bits),
                                  (_lib.PBVD_TERMINATED if terminated else 0)
-                                 | (_lib.PBVD_ALLOW_CATASTROPHIC if allow_catastrophic else 0),
+                                 | (_lib.PBVD_ALLOW_CATASTROPHIC if allow_catastrophic else 0)
+                                 | (_lib.PBVD_START_ZERO if start_zero else 0),
                                  self.device)
         _check(rc, None, "pbvd_create")
         self._h = h

@@ -54,3 +54,27 @@ def test_gpu_ber_fig4_trend_in_L(P):
         assert b <= a * 1.15, bers          # non-increasing up to sampling noise
     assert bers[0] > 1.2 * bers[-1], bers   # L = 7 is not converged
     assert abs(bers[3] - bers[4]) <= 0.15 * bers[4], bers   # L = 42 ~ L = 63
+
+
+def test_gpu_ber_fig4_s0_versus_min_pm(P):
+    """Fig. 4 with the paper's own traceback start ("state S_0", Alg. 1
+    K2 state = 0; PBVD_START_ZERO) beside the min-PM start on
+    the same frames at 3 dB: S_0 needs a longer L -- far worse at L = 7
+    (4.8e-3 vs 5.5e-4), non-increasing in L, and equal to
+    the min-PM BER by L = 63 within sampling noise.  The first 64 blocks of
+    each point are checked bit for bit against the oracle on the same frames."""
+    B = _tools()
+    code = synth.CODES["k7"]
+    res = {}
+    for L in (7, 14, 28, 63):
+        for sz in (False, True):
+            d = B.ber_point(P, code, 3.0, 512, L, 1 << 24, seed=321, start_zero=sz,
+                            oracle_blocks=64, detail=True)
+            assert d["oracle_blocks_bit_exact"], (L, sz)
+            res[(L, sz)] = d["ber"]
+    s0 = [res[(L, True)] for L in (7, 14, 28, 63)]
+    mp = [res[(L, False)] for L in (7, 14, 28, 63)]
+    assert s0[0] > 4 * mp[0], (s0, mp)
+    for a, b in zip(s0, s0[1:]):
+        assert b <= a * 1.15, s0
+    assert abs(s0[-1] - mp[-1]) <= 0.2 * mp[-1], (s0, mp)

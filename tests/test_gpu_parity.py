@@ -26,9 +26,10 @@ def pbvd():
     return P
 
 
-def gpu_decode(P, code, llr, n_info, D, L, punct=None, terminated=True, lanes=0, fused=True):
+def gpu_decode(P, code, llr, n_info, D, L, punct=None, terminated=True, lanes=0, fused=True,
+               start_zero=False):
     dec = P.Decoder(code["K"], code["polys"], D, L, punct=punct, terminated=terminated,
-                    lanes=lanes, fused=fused)
+                    lanes=lanes, fused=fused, start_zero=start_zero)
     d = llr.to("cuda") if not llr.is_cuda else llr
     out = dec.decode(d, n_info)
     torch.cuda.synchronize()
@@ -107,6 +108,43 @@ def test_L_multiple_of_D(pbvd, orc, K, D, L):
         for fused in (True, False):
             got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, fused=fused)
             assert (got == want).all(), (seed, fused, np.nonzero(got != want)[0][:8])
+
+
+@pytest.mark.parametrize("cfg", SMALL[:11], ids=lambda c: "-".join(map(str, c)))
+def test_start_zero_bit_exact(pbvd, orc, cfg):
+    """PBVD_START_ZERO, the paper's own traceback start (P:93 "state S_0";
+    Alg. 1 K2 state = 0): every block traces back from state 0.  Against
+    the oracle's START_ZERO (pinned in tests/test_oracle.py)."""
+    name, pk, hard, n_info, D, L, term, ebn0 = cfg
+    code, punct = synth.CODES[name], synth.PUNCT[pk]
+    info, llr = synth.make_stream(code, n_info, ebn0 - 2.0, 23, punct, hard, term)
+    flags = (orc.TERMINATED if term else 0) | orc.START_ZERO
+    want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, D, L, flags=flags, punct=punct))
+    for lanes in lane_variants(pbvd, code):
+        for fused in (True, False):
+            got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, punct, term, lanes, fused,
+                                start_zero=True)
+            bad = np.nonzero(got != want)[0]
+            assert bad.size == 0, (lanes, fused, bad[:8])
+
+
+@pytest.mark.parametrize("K,D,L", [(7, 64, 6), (7, 64, 10), (9, 128, 8), (3, 32, 3)])
+def test_start_zero_differs_from_min_pm(pbvd, orc, K, D, L):
+    """At short L and low SNR the two traceback starts give different bits
+    (Fig. 4's S_0 curve lies above the min-PM one), so
+    the flag is really taken -- and each GPU start equals the oracle's."""
+    code = synth.CODES[{3: "k3", 7: "k7", 9: "k9"}[K]]
+    n_info = 40 * D
+    info, llr = synth.make_stream(code, n_info, 1.0, 77)
+    outs = {}
+    for sz in (False, True):
+        flags = orc.TERMINATED | (orc.START_ZERO if sz else 0)
+        want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, D, L, flags=flags))
+        for fused in (True, False):
+            got, _ = gpu_decode(pbvd, code, llr, n_info, D, L, fused=fused, start_zero=sz)
+            assert (got == want).all(), (sz, fused)
+        outs[sz] = want
+    assert (outs[True] != outs[False]).any()
 
 
 def test_saturated_and_extreme_inputs(pbvd, orc):
