@@ -43,7 +43,9 @@ def load(path: os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # PBVD_LIB: an alternative build of the same library (A/B experiments,
+    # tools/ only); the default is the in-tree libpbvd.so
+    p = Path(path) if path else Path(os.environ.get("PBVD_LIB", str(LIB_PATH)))
     if not p.exists():
         raise ImportError(f"{p} not found: build the CUDA library first "
                           "(python -m paper_1608_00066_b200.build); there is no CPU fallback")

@@ -54,9 +54,6 @@
 #ifndef PBVD_DSCHEME
 #define PBVD_DSCHEME 1
 #endif
-#ifndef PBVD_DIRECT_SOFT
-#define PBVD_DIRECT_SOFT 0
-#endif
 #ifndef PBVD_SKIP_ROWS
 #define PBVD_SKIP_ROWS 0
 #endif
@@ -95,6 +92,9 @@
 #endif
 #ifndef PBVD_CYCLE_PREFETCH
 #define PBVD_CYCLE_PREFETCH 1
+#endif
+#ifndef PBVD_NODEC_WARMUP
+#define PBVD_NODEC_WARMUP 0
 #endif
 
 namespace pbvd {
@@ -170,11 +170,7 @@ struct Cfg {
     }
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
-    // R = 2: the ACS loop reads each stage's two soft bytes of both blocks
-    // straight from the (2-byte aligned) raw / depunctured windows -- no
-    // transform pass and no operand buffer
-    static constexpr bool DIRECT = (R == 2) && PBVD_DIRECT_SOFT;
-    static constexpr size_t WLAM = DIRECT ? 0 : size_t(2) * PPW * LSTR * 4;   // double buffered
+    static constexpr size_t WLAM = size_t(2) * PPW * LSTR * 4;   // double buffered
     static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
     static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
@@ -229,26 +225,11 @@ __device__ __forceinline__ XY<CF> load_xy(const uint32_t* lamrow, int s) {
     return r;
 }
 
-// Soft-value source of the ACS loop: the transformed per-pair words (lam
-// row), or -- DIRECT, R = 2 -- the two blocks' windows read in place: one
-// 16-bit load per block, interleaved [uA0, uB0, uA1, uB1] and biased by PRMT
-// and one XOR.
+// Soft-value source of the ACS loop: the transformed per-pair words (lam row)
 template <class CF>
 struct SoftSrc {
     const uint32_t* lamrow = nullptr;
-    const uint8_t* a = nullptr;          // stage 0 of the chunk, block A window
-    const uint8_t* b = nullptr;          // same, block B
-    __device__ __forceinline__ XY<CF> load(int s) const {
-        if constexpr (CF::DIRECT) {
-            XY<CF> r;
-            const uint32_t x = *reinterpret_cast<const uint16_t*>(a + 2 * s);
-            const uint32_t y = *reinterpret_cast<const uint16_t*>(b + 2 * s);
-            r.v[0] = prmt(x, y, 0x5140u) ^ 0x80808080u;
-            return r;
-        } else {
-            return load_xy<CF>(lamrow, s);
-        }
-    }
+    __device__ __forceinline__ XY<CF> load(int s) const { return load_xy<CF>(lamrow, s); }
 };
 
 // The 2^R codeword metrics of one stage for a block pair, permuted by the
@@ -502,10 +483,58 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
     }
 }
 
+// One trellis stage WITHOUT decisions (Eq. 1's min only): the stages below
+// the first survivor row any traceback reads (s < t0r + v, the truncated
+// block's warm-up) need the path metrics but no survivor bits, so the
+// decision operand, its packing and the store are skipped -- 2 instructions
+// per output register instead of ~4.4.
+template <class CF, int P>
+__device__ __forceinline__ void acs_stage_nodec(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
+                                                int lg) {
+    using C = typename CF::code;
+    constexpr int S = CF::S, NC = CF::NC;
+    constexpr int g0 = C::g0, gK = C::gK;
+    if constexpr (P < CF::LB) {
+        uint32_t Pv[NC];
+        bm_vector<CF, CF::lane_possible(P)>(xy, flip, Pv);
+        constexpr int pb = 1 << P;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            if (k & pb) continue;
+            const int a = CF::alpha_reg(k, P);
+            const uint32_t E = pm[k], O = pm[k | pb];
+            pm[k] = __viaddmin_s16x2(E, Pv[a], add32(O, Pv[a ^ g0]));             // Eqs. 3, 5
+            pm[k | pb] = __viaddmin_s16x2(E, Pv[a ^ gK], add32(O, Pv[a ^ gK ^ g0]));  // Eqs. 4, 6
+        }
+    } else {
+        constexpr int li = P - CF::LB;
+        const uint32_t lb = uint32_t(lg >> li) & 1u;
+        uint32_t recv[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) recv[k] = __shfl_xor_sync(0xffffffffu, pm[k], 1 << li);
+        uint32_t Po[NC], Pr[NC];
+        if constexpr (C::symmetric) {
+            bm_vector<CF, CF::lane_possible(P)>(xy, flip, Po);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) Pr[c] = Po[c ^ C::ALL];
+        } else {
+            const int fo = flip ^ (lb ? (gK ^ g0) : 0);
+            const int fr = flip ^ (lb ? gK : g0);
+            bm_vector<CF, CF::lane_possible(P) | (gK ^ g0)>(xy, fo, Po);
+            bm_vector<CF, CF::lane_possible(P) | gK | g0>(xy, fr, Pr);
+        }
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const int a = CF::alpha_reg(k, P);
+            pm[k] = __viaddmin_s16x2(pm[k], Po[a], add32(recv[k], Pr[a]));
+        }
+    }
+}
+
 // v stages at phases P..v-1, the operands of stage P+1 loaded one stage ahead
 // (one basic block: the scheduler overlaps stage P+1's loads and branch
 // metrics with stage P's butterflies).
-template <class CF, int P, bool FULL>
+template <class CF, int P, bool FULL, bool DEC = true>
 struct Cycle {
     static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const SoftSrc<CF>& src,
                                                const int (&flip)[CF::V], int lg, uint32_t* drow,
@@ -516,12 +545,15 @@ struct Cycle {
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst) nxt = src.load(s0 + P + 1);
             }
-            acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW,
-                             !PBVD_SKIP_ROWS || s0 + P >= st_lo, one, neg1);
+            if constexpr (DEC)
+                acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW,
+                                 !PBVD_SKIP_ROWS || s0 + P >= st_lo, one, neg1);
+            else
+                acs_stage_nodec<CF, P>(pm, cur, flip[P], lg);
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst)
-                    Cycle<CF, P + 1, FULL>::run(pm, src, flip, lg, drow, s0, nst, st_lo, nxt, one,
-                                                neg1);
+                    Cycle<CF, P + 1, FULL, DEC>::run(pm, src, flip, lg, drow, s0, nst, st_lo, nxt,
+                                                     one, neg1);
             }
         }
     }
@@ -535,7 +567,12 @@ __device__ __forceinline__ void init_flips(int (&flip)[CF::V], int lg,
 
 __device__ __forceinline__ int64_t kept_before(const FwdParams& p, int64_t s, int R) {
     if (p.P == 1) return s * R;
-    return (s / p.P) * p.kp + p.cum[s % p.P];
+    // floor division: the erasure pad of the first interior block may start
+    // before stage 0 (those bytes are outside the window and zero-filled)
+    int64_t q = s / p.P;
+    int r = int(s - q * p.P);
+    if (r < 0) { r += p.P; --q; }
+    return q * p.kp + p.cum[r];
 }
 
 // MIRROR (fused only): after its walk each warp also copies its decoded bytes
@@ -580,7 +617,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         if (edge) return p.edges[e].lo;
         int64_t bi = wb0 + i;
         if (bi >= p.n_int) bi = p.n_int - 1;
-        return (p.b_int0 + bi) * p.D - p.L;
+        return (p.b_int0 + bi) * p.D - p.L - p.pad;
     };
     const int nblk = edge ? 1 : BPW;
     const uintptr_t vlo = reinterpret_cast<uintptr_t>(p.llr);
@@ -652,7 +689,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             const int woff = win_off(i, a);
             const uint32_t* win = reinterpret_cast<const uint32_t*>(rb + size_t(CF::wslot(i)) * RAWB);
             uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(CF::wslot(i)) * RAWB);
-            const uint32_t* tab = p.dtab + int(a % p.P) * NWD;
+            const uint32_t* tab = p.dtab + int(((a % p.P) + p.P) % p.P) * NWD;
             const int nw = (nst * R + 3) / 4;
 #pragma unroll 4
             for (int w = 0; w < nw; ++w) {
@@ -668,7 +705,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             const int64_t a = block_lo(i) + s0;
             const uint8_t* src = rb + size_t(CF::wslot(i)) * RAWB + win_off(i, a);
             uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(CF::wslot(i)) * RAWB);
-            int ph = int(a % p.P), idx = 0, nb = 0;
+            int ph = int(((a % p.P) + p.P) % p.P), idx = 0, nb = 0;
             uint32_t acc = 0;
             for (int st = 0; st < nst; ++st) {
 #pragma unroll
@@ -784,9 +821,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         gdec = p.dec_edge + size_t(e) * size_t(p.span_edge_max) * ROW;
     }
 
-    if constexpr (CF::DIRECT) {
-        issue_raw(0);
-    } else {
+    {
         issue_raw(0);
         if (nchunks > 1) issue_raw(1);
         if (nchunks > 1) cp_async_wait<1>(); else cp_async_wait<0>();
@@ -798,27 +833,18 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
 #pragma unroll 1
         for (int j = 0; j < CF::NCYC; ++j) transform(0, j);
         __syncwarp();
+        if (!edge && p.pad > 0) {
+            // the front pad stages are erasures (lambda = 0, biased u = 128)
+            const int n = p.pad * LW;
+            for (int i = lane; i < PPW * n; i += 32) lam[(i / n) * LSTR + i % n] = 0x80808080u;
+            __syncwarp();
+        }
     }
     for (int c = 0; c < nchunks; ++c) {
         const int nst = min(T, span - c * T);
         const bool next = c + 1 < nchunks;
         SoftSrc<CF> src;
-        if constexpr (CF::DIRECT) {
-            // chunk c's windows (issued a chunk ago) land; chunk c+1's go in
-            // flight into the other buffer (chunk c-1, its reader, is done)
-            cp_async_wait<0>();
-            __syncwarp();
-            if (next) issue_raw(c + 1);
-            const bool dense = (p.P == 1);
-            if (!dense) {
-                depuncture(c);
-                __syncwarp();
-            }
-            const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
-            const int iA = edge ? 0 : 2 * grp, iB = edge ? 0 : 2 * grp + 1;
-            src.a = rb + size_t(CF::wslot(iA)) * RAWB + (dense ? woffs[(c & 1) * BPW + iA] : 0);
-            src.b = rb + size_t(CF::wslot(iB)) * RAWB + (dense ? woffs[(c & 1) * BPW + iB] : 0);
-        } else {
+        {
             // soft windows of chunk c+2 go in flight; those of chunk c+1 (issued a
             // chunk ago) must have landed before this chunk's transform slices
             if (c + 2 < nchunks) {
@@ -838,13 +864,29 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         // each warp writes 32 * WPS contiguous words per stage)
         uint32_t* drow = gdec + size_t(c) * T * ROW + size_t(lane) * CF::WPS;
         const int st_lo = s_read - c * T;     // rows below the traceback's first row: no store
-        if (nst == T) {
+        // whole v-stage cycles of the chunk run in the one hot loop (interior
+        // spans are padded to a multiple of v); only an edge block's last
+        // chunk can leave a remainder of < v stages
+        const int ncyc = nst / V;
+        {
             // each cycle's first-stage operands are loaded one cycle ahead
             // (within a cycle Cycle<> loads one stage ahead); the read past the
             // chunk's last stage stays inside the operand row's padding
             XY<CF> first = src.load(0);
+            // cycles wholly below the first survivor row the traceback reads:
+            // path metrics only (acs_stage_nodec)
+            const int jd = PBVD_NODEC_WARMUP ? min(ncyc, max(0, st_lo / V)) : 0;
 #pragma unroll 1
-            for (int j = 0; j < CF::NCYC; ++j) {
+            for (int j = 0; j < jd; ++j) {
+                const int s0 = j * V;
+                const XY<CF> nfirst = src.load(s0 + V);
+                Cycle<CF, 0, true, false>::run(pm, src, flip, lg, drow, s0, T, st_lo, first, p.one,
+                                               p.neg_one);
+                first = nfirst;
+                transform(c + 1, j);
+            }
+#pragma unroll 1
+            for (int j = jd; j < ncyc; ++j) {
                 const int s0 = j * V;
 #if PBVD_CYCLE_PREFETCH
                 const XY<CF> nfirst = src.load(s0 + V);
@@ -855,25 +897,12 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                 Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, T, st_lo, src.load(s0),
                                         p.one, p.neg_one);
 #endif
-                if constexpr (!CF::DIRECT) transform(c + 1, j);     // harmless past the last chunk
-            }
-        } else {
-            // partial (last) chunk: whole cycles unguarded, then the remainder
-            int s0 = 0;
-#pragma unroll 1
-            for (; s0 + V <= nst; s0 += V)
-                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, nst, st_lo, src.load(s0),
-                                        p.one, p.neg_one);
-            if (s0 < nst)
-                Cycle<CF, 0, false>::run(pm, src, flip, lg, drow, s0, nst, st_lo, src.load(s0),
-                                         p.one, p.neg_one);
-            if constexpr (!CF::DIRECT) {
-                if (next) {
-#pragma unroll 1
-                    for (int j = 0; j < CF::NCYC; ++j) transform(c + 1, j);
-                }
+                transform(c + 1, j);     // harmless past the last chunk
             }
         }
+        if (ncyc * V < nst)   // (the last chunk of an edge block)
+            Cycle<CF, 0, false>::run(pm, src, flip, lg, drow, ncyc * V, nst, st_lo,
+                                     src.load(ncyc * V), p.one, p.neg_one);
         // renormalise: subtract the block minimum (per 16-bit half = per block)
         uint32_t mn = pm[0];
 #pragma unroll

@@ -24,7 +24,6 @@ void fill_shape(Variant& v) {
     for (int r = 0; r < 4; ++r) v.polys[r] = r < C::R ? C::g(r) : 0;
     v.BPC = CF::BPC;
     v.BOXB = CF::BOXB;
-    v.direct = CF::DIRECT;
     v.BPW = CF::BPW;
     v.NT = CF::NT;
     v.T = CF::T;

@@ -55,7 +55,8 @@ struct FwdParams {
     int n_int;             // interior blocks in this launch
     int n_int_warps;       // warp units for interior blocks; edge units follow
     int D, L;
-    int span_int;          // D + 2L
+    int span_int;          // D + 2L + pad (interior forward stages)
+    int pad;               // interior spans start `pad` erasure stages early (a multiple of v)
     uint32_t one, neg_one; // 1 and 0xffffffff, opaque to the compiler (pipe balancing)
     int P;                 // puncture period (1 = none)
     int kp;                // kept values per period

@@ -41,8 +41,6 @@ using namespace pbvd;
 struct Workspace {
     void* p = nullptr;
     size_t bytes = 0;
-    void* al = nullptr;       // realigned soft window (odd caller pointers only)
-    size_t al_bytes = 0;
 };
 
 // Resources of the host-buffer pipeline (pbvd_decode_host): per stream a
@@ -115,13 +113,32 @@ int64_t kept_before_h(const pbvd_s* h, int64_t s) {
     return (s / h->P) * h->kp + h->cum[s % h->P];
 }
 
+// Dynamic shared memory of a forward / fused launch: the variant's need, or
+// more, so that at most FWD_WARPS_PER_SM one-warp CTAs are resident per SM
+// (228 KB of shared memory per SM, 1 KB reserved per CTA).  Measured on B200
+// (tools/r2f.sh): 3 warps per SM sub-partition beat 4 by 10 % at 2^26 bits
+// (C2 119 vs 109 Gb/s, C3a 106 vs 97) -- more resident warps spread over
+// more code (hot loop, traceback, prologue) and miss in the 32 KB
+// instruction cache -- and 2 per sub-partition lose again (112).
+// PBVD_FWD_WARPS_PER_SM overrides it (0 = no cap) for experiments.
+constexpr int FWD_WARPS_PER_SM = 12;
+size_t fwd_smem(size_t need) {
+    static const int cap = [] {
+        const char* e = std::getenv("PBVD_FWD_WARPS_PER_SM");
+        return e ? std::atoi(e) : FWD_WARPS_PER_SM;
+    }();
+    if (cap <= 0) return need;
+    const size_t per = ((size_t(228) * 1024 / size_t(cap) - 1024) / 128) * 128;
+    return std::max(need, per);
+}
+
 int ensure_prepared(pbvd_t h, const Variant* v) {
     std::lock_guard<std::mutex> lk(g_prep_mu);
     const uint64_t bit = uint64_t(1) << (h->device & 63);
     if (!(v->prepared & bit)) {
-        const std::pair<const void*, size_t> ks[4] = {{v->k_fwd, v->smem_fwd},
-                                                       {v->k_fused, v->smem_fused},
-                                                       {v->k_mirror, v->smem_fused},
+        const std::pair<const void*, size_t> ks[4] = {{v->k_fwd, fwd_smem(v->smem_fwd)},
+                                                       {v->k_fused, fwd_smem(v->smem_fused)},
+                                                       {v->k_mirror, fwd_smem(v->smem_fused)},
                                                        {v->k_tb, v->smem_tb}};
         for (const auto& k : ks) {
             cudaError_t e = cudaFuncSetAttribute(k.first, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -215,17 +232,6 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     }
     int rc = ensure_prepared(h, v);
     if (rc) return rc;
-    if (v->direct && h->P == 1 && (reinterpret_cast<uintptr_t>(llr) & 1)) {
-        // the forward kernel reads each stage's two soft bytes with one
-        // 16-bit load: an odd caller pointer is realigned through a copy
-        const size_t nb2 = size_t(n_llr_win);
-        rc = ensure_buf(h, &W.al, &W.al_bytes, nb2);
-        if (rc) return rc;
-        cudaError_t e = cudaMemcpyAsync(W.al, llr, nb2, cudaMemcpyDeviceToDevice, stream);
-        if (e != cudaSuccess) return cuda_fail(h, e, "realign copy");
-        llr = static_cast<const int8_t*>(W.al);
-    }
-
     // interior blocks: lo = bD - L > 0 (a span starting at stage 0 is a head
     // block with the known start state, reading c-12), b < nb-1,
     // (b+1)D + L <= n_stages
@@ -253,7 +259,15 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     for (const auto& e : edges) span_edge_max = std::max(span_edge_max, e.span);
 
     // ---- workspace: one wave of interior survivors + edge survivors + starts
-    const int span_int = int(D + 2 * L);
+    // interior spans are padded at the FRONT with `pad` erasure stages so
+    // their length is a multiple of v: every chunk then runs whole v-stage
+    // cycles of the one hot loop (no separate partial-chunk code -- which
+    // thrashed the instruction cache).  With all-equal initial metrics and
+    // lambda = 0 every stage adds the same BM' to every state, so the
+    // metrics at the true span start are still all equal (reading c-11):
+    // the decisions read by the traceback are unchanged.
+    const int pad = int((h->V - (D + 2 * L) % h->V) % h->V);
+    const int span_int = int(D + 2 * L) + pad;
     const size_t region_bytes = size_t(span_int) * v->ROW * 4;      // BPW blocks
     const int64_t n_int = I1 - I0;
     const size_t edge_region_bytes = size_t(span_edge_max) * v->ROW * 4;
@@ -303,16 +317,17 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     fp.out = out;
     fp.n_mirror = h->fused ? h->n_mirror : 0;
     for (int k = 0; k < MAX_MIRROR; ++k) fp.mirror[k] = h->mirror[k];
-    fp.t0r = int(L);
-    fp.t1r = int(L + D);
+    fp.t0r = int(L) + pad;
+    fp.t1r = int(L + D) + pad;
+    fp.pad = pad;
     fp.start_zero = (h->flags & PBVD_START_ZERO) ? 1 : 0;
 
     TbParams tp{};
     tp.dec = dec_int;
     tp.start = start_int;
     tp.span_int = span_int;
-    tp.t0r = int(L);
-    tp.t1r = int(L + D);
+    tp.t0r = int(L) + pad;
+    tp.t1r = int(L + D) + pad;
     tp.D = int(D);
     tp.out = out;
     tp.dec_edge = dec_edge;
@@ -413,8 +428,9 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         }
 #endif
         cudaError_t le = h->fused ? launch(fp.n_mirror > 0 ? v->k_mirror : v->k_fused, fgrid, v->NT,
-                                           v->smem_fused, stream, fp, false)
-                                  : launch(v->k_fwd, fgrid, v->NT, v->smem_fwd, stream, fp, false);
+                                           fwd_smem(v->smem_fused), stream, fp, false)
+                                  : launch(v->k_fwd, fgrid, v->NT, fwd_smem(v->smem_fwd), stream, fp,
+                                           false);
         if (le != cudaSuccess) return cuda_fail(h, le, "forward kernel launch");
 #ifdef PBVD_EXP_TIMING
         if (dump) {
@@ -622,10 +638,8 @@ void pbvd_destroy(pbvd_t h) {
         DeviceGuard g(h->device);
         if (h->dtab) cudaFree(h->dtab);
         if (h->ws.p) cudaFree(h->ws.p);
-        if (h->ws.al) cudaFree(h->ws.al);
         for (auto& ln : h->lanes) {
             if (ln.ws.p) cudaFree(ln.ws.p);
-            if (ln.ws.al) cudaFree(ln.ws.al);
             if (ln.d_llr) cudaFree(ln.d_llr);
             if (ln.d_bits) cudaFree(ln.d_bits);
             if (ln.stream) cudaStreamDestroy(ln.stream);

@@ -183,10 +183,13 @@ __device__ __forceinline__ uint32_t row_bit_at(RowT<CF> b, uint32_t q, uint32_t 
         return y;
     }
 }
+// the v steps of a cycle (phases v-1 .. 0): each replaces bit PH of q by the
+// survivor bit it reads, so after the cycle q itself holds the cycle's v
+// survivor bits in step order (bit 0 = newest) -- the output accumulator
+// takes them in one shift-or per cycle (tbc_cycle), not one per step
 template <class CF, int PH>
 __device__ __forceinline__ void tbc_steps(TbState& t, const RowT<CF> (&b)[CF::V], uint32_t hbit) {
     const uint32_t xs = row_bit_at<CF, PH>(b[PH], t.q, hbit);
-    t.acc64 = (t.acc64 << 1) | ((xs >> PH) & 1u);
     t.q = bit_insert<1u << PH>(t.q, xs);
     if constexpr (PH > 0) tbc_steps<CF, PH - 1>(t, b, hbit);
 }
@@ -204,6 +207,7 @@ __device__ __forceinline__ void tbc_cycle(TbState& t, const uint32_t* row, int w
     RowT<CF> b[CF::V];
     tbc_load<CF, CF::V - 1>(b, row, woff, sel);
     tbc_steps<CF, CF::V - 1>(t, b, hbit);
+    t.acc64 = (t.acc64 << CF::V) | t.q;
     const int eb = t.e, ea = t.e - CF::V;
     const int w = eb >> 5;
     if (eb >= 0 && (w << 5) > ea && w < nwords)

@@ -21,7 +21,6 @@ struct Variant {
     uint32_t polys[4];
     int BPC, BPW, NT, T, ROW, NR_TB, TT, BOXB;
     int NT_TB;          // threads per traceback CTA
-    bool direct;        // reads R = 2 soft bytes with 16-bit loads: needs an even llr address
     size_t smem_fwd, smem_tb, smem_fused;
     int default_rank;   // lower = preferred default for the code
     bool jit;           // built at run time by NVRTC (jit.cu)
