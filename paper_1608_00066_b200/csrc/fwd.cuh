@@ -50,51 +50,18 @@
 #include "ptx.cuh"
 #include "tb.cuh"
 
-// compile-time experiment switches (defaults are the measured best)
-#ifndef PBVD_DSCHEME
-#define PBVD_DSCHEME 1
-#endif
-#ifndef PBVD_SKIP_ROWS
-#define PBVD_SKIP_ROWS 0
-#endif
+// compile-time tunables (defaults are the measured best; DESIGN.md §7 lists
+// the alternatives that were measured and removed)
 #ifndef PBVD_MAXREG
 #define PBVD_MAXREG 200
 #endif
 #ifndef PBVD_MAXREG_S64
 #define PBVD_MAXREG_S64 200
 #endif
-#ifndef PBVD_L2_HINTS
-#define PBVD_L2_HINTS 0
-#endif
-#ifndef PBVD_DEC_HINT
-#define PBVD_DEC_HINT 1
-#endif
-#ifndef PBVD_IN_HINT
-#define PBVD_IN_HINT 0
-#endif
-#ifndef PBVD_PACK_TREE
-#define PBVD_PACK_TREE 0
-#endif
-#ifndef PBVD_FMA_SPLIT
-#define PBVD_FMA_SPLIT 1
-#endif
-#ifndef PBVD_PACK_IMAD
-#define PBVD_PACK_IMAD 0
-#endif
-#ifndef PBVD_DMIX
-#define PBVD_DMIX 0
-#endif
-#ifndef PBVD_DEP_TABLE
-#define PBVD_DEP_TABLE 1
-#endif
-#ifndef PBVD_WSLOT_HMAJOR
-#define PBVD_WSLOT_HMAJOR 1
-#endif
-#ifndef PBVD_CYCLE_PREFETCH
-#define PBVD_CYCLE_PREFETCH 1
-#endif
-#ifndef PBVD_NODEC_WARMUP
-#define PBVD_NODEC_WARMUP 0
+// survivor rows staged in shared memory and written by cp.async.bulk (one
+// bulk copy per v-stage cycle) instead of direct 8-byte stores per lane
+#ifndef PBVD_BULK_STORE
+#define PBVD_BULK_STORE 0
 #endif
 
 namespace pbvd {
@@ -166,13 +133,16 @@ struct Cfg {
     // warp's 32-bit transform reads hit 8 banks instead of 4 (a 16-byte
     // aligned window start can only reach banks = 0 mod 4)
     __host__ __device__ static constexpr int wslot(int i) {
-        return PBVD_WSLOT_HMAJOR ? (i & 1) * PPW + (i >> 1) : i;
+        return (i & 1) * PPW + (i >> 1);
     }
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
     static constexpr size_t WLAM = size_t(2) * PPW * LSTR * 4;   // double buffered
     static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
-    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128;
+    // PBVD_BULK_STORE: NSTG slots of one v-stage cycle of survivor rows
+    static constexpr int NSTG = 4;
+    static constexpr size_t WSTG = PBVD_BULK_STORE ? size_t(NSTG) * V * ROW * 4 : 0;
+    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128 + WSTG;
     static constexpr size_t SMEM = NWARP * WSMEM;
 
     // alpha of the butterfly whose E slot has register index k, restricted
@@ -270,7 +240,7 @@ __device__ __forceinline__ void bm_vector(const XY<CF>& xy, int flip, uint32_t (
 // store them to this lane's shared-memory row.  Bit layout of word kw:
 // slot q_reg = 16*kw + (b & 15) of block half (b >> 4)   (S >= 16), or
 // bit = 16*h + 8*(q_reg / (S/2)) + q_reg % (S/2)         (S < 16).
-template <class CF>
+template <class CF, bool BULK = false>
 __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t inv,
                                            uint32_t* drow, bool st) {
     constexpr int S = CF::S, WPS = CF::WPS;
@@ -279,37 +249,6 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
     if constexpr (S >= 16) {
 #pragma unroll
         for (int kw = 0; kw < WPS; ++kw) {
-#if PBVD_PACK_TREE
-            // P_m: bytes = sign of [t(m).A, t(8+m).A, t(m).B, t(8+m).B] (0x00/0xFF)
-            uint32_t P[8];
-#pragma unroll
-            for (int m = 0; m < 8; ++m) P[m] = prmt(t[16 * kw + m], t[16 * kw + 8 + m], SEL);
-            // bit m of every byte from P_m: a 3-level LOP3 tree (depth 3, 7 ops)
-            uint32_t w2[4], w4[2];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t M = 0x01010101u << (2 * i);       // bit 2i from P[2i]
-                w2[i] = (P[2 * i] & M) | (P[2 * i + 1] & ~M);
-            }
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const uint32_t M = 0x03030303u << (4 * i);       // bits 4i,4i+1 from w2[2i]
-                w4[i] = (w2[2 * i] & M) | (w2[2 * i + 1] & ~M);
-            }
-            words[kw] = ((w4[0] & 0x0F0F0F0Fu) | (w4[1] & 0xF0F0F0F0u)) ^ inv;
-#elif PBVD_PACK_IMAD
-            // P_m: bytes 0x00/0xFF (signs as below).  sum_m 2^m P_m = 255 X where
-            // byte j of X has bit m = sign byte j of P_m, so X = sum_m P_m *
-            // (2^m / 255 mod 2^32): 8 IMADs on the FMA pipe instead of 7 LOP3s
-            // on the ALU pipe (1/255 mod 2^32 = 0xFEFEFEFF)
-            uint32_t acc = 0;
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const uint32_t pm = prmt(t[16 * kw + m], t[16 * kw + 8 + m], SEL);
-                acc = imad(pm, 0xFEFEFEFFu << m, acc);
-            }
-            words[kw] = acc ^ inv;
-#else
             // P_m: bytes = sign of [t(m).A, t(8+m).A, t(m).B, t(8+m).B] (0x00/0xFF);
             // bit m of every byte from P_m by a chain of LOP3 merges
             uint32_t wd = prmt(t[16 * kw], t[16 * kw + 8], SEL);
@@ -320,7 +259,7 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
                 wd = (wd & M) | (pm & ~M);
             }
             words[kw] = wd ^ inv;
-#endif
+
         }
     } else {
         constexpr int H = S / 2;
@@ -333,11 +272,24 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
         }
         words[0] = (wd ^ inv) & (0x01010101u * ((1u << H) - 1u));
     }
+    if constexpr (BULK) {
+        // drow: this lane's words of the row in the shared-memory staging slot
+        if constexpr (WPS == 1) {
+            drow[0] = words[0];
+        } else if constexpr (WPS == 2) {
+            *reinterpret_cast<uint2*>(drow) = make_uint2(words[0], words[1]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < WPS; i += 4)
+                *reinterpret_cast<uint4*>(drow + i) =
+                    make_uint4(words[i], words[i + 1], words[i + 2], words[i + 3]);
+        }
+        return;
+    }
     if (!st) return;       // a row the traceback never reads (below its first row)
-#if PBVD_DEC_HINT
     // survivor stores with an L2 eviction-priority hint (the fused traceback
     // re-reads them from L2)
-    const uint64_t pol = PBVD_DEC_HINT == 1 ? policy_evict_last_nv() : policy_evict_first_nv();
+    const uint64_t pol = policy_evict_last_nv();
     if constexpr (WPS == 1) {
         st_global_hint(drow, words[0], pol);
     } else if constexpr (WPS == 2) {
@@ -347,18 +299,7 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
         for (int i = 0; i < WPS; i += 4)
             st_global_v4_hint(drow + i, words[i], words[i + 1], words[i + 2], words[i + 3], pol);
     }
-#else
-    if constexpr (WPS == 1) {
-        drow[0] = words[0];
-    } else if constexpr (WPS == 2) {
-        *reinterpret_cast<uint2*>(drow) = make_uint2(words[0], words[1]);
-    } else {
-#pragma unroll
-        for (int i = 0; i < WPS; i += 4)
-            *reinterpret_cast<uint4*>(drow + i) =
-                make_uint4(words[i], words[i + 1], words[i + 2], words[i + 3]);
-    }
-#endif
+
 }
 
 // One trellis stage at compile-time phase P (Eq. 1 per output state).
@@ -368,16 +309,10 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
 // which also carries VIADDMNMX, PRMT and LOP3 -- is not the only one busy.
 template <class CF>
 __host__ __device__ constexpr bool fma_out(int k) {
-    return PBVD_FMA_SPLIT == 0 ? false : PBVD_FMA_SPLIT == 1 ? (k & 1) != 0 : (k % 3) != 0;
+    return (k & 1) != 0;
 }
 
-// butterfly k (lower index) of phase P uses the IADD3 decision operands
-__host__ __device__ constexpr bool dmix_iadd3(int k, int P) {
-    // rank of k among the butterflies of the stage (k with bit P cleared)
-    return PBVD_DMIX > 0 && ((((k >> (P + 1)) << P) | (k & ((1 << P) - 1))) % 4) < PBVD_DMIX;
-}
-
-template <class CF, int P>
+template <class CF, int P, bool BULK = false>
 __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
                                           int lg, uint32_t* drow, bool st, uint32_t one,
                                           uint32_t neg1) {
@@ -392,7 +327,7 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
 #pragma unroll
         for (int c = 0; c < NC; ++c) PC[c] = add32(Pv[c], 0x7FFF7FFFu);
         constexpr int pb = 1 << P;
-        if constexpr (PBVD_DSCHEME && NC <= 4) {
+        if constexpr (NC <= 4) {
         // d-scheme: t = (E - O) + (PC_own - BM_other), the same 32-bit sum as
         // E - m_other + PC_own, with E - O shared by the butterfly's two
         // outputs and every add two-operand (either pipe): 3.5 instructions
@@ -413,18 +348,11 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             const uint32_t nO = __viaddmin_s16x2(E, Pv[a ^ gK], mO1);
             pm[k] = nE;
             pm[k | pb] = nO;
-            // butterfly index within the stage: the first PBVD_DMIX of every 4
-            // take one IADD3 per output (ALU) instead of the shared-d pair
-            if (dmix_iadd3(k, P)) {
-                t[k] = sub_add(E, mO0, PC[a]);
-                t[k | pb] = sub_add(E, mO1, PC[a ^ gK]);
-            } else {
-                const uint32_t d = imad(O, neg1, E);
-                t[k] = add32(d, KC[a]);
-                t[k | pb] = add32(d, KC[a ^ gK]);
-            }
+            const uint32_t d = imad(O, neg1, E);
+            t[k] = add32(d, KC[a]);
+            t[k | pb] = add32(d, KC[a ^ gK]);
         }
-        pack_store<CF>(t, 0u, drow, st);
+        pack_store<CF, BULK>(t, 0u, drow, st);
         return;
         }
 #pragma unroll
@@ -447,7 +375,7 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             t[k] = tE;
             t[k | pb] = tO;
         }
-        pack_store<CF>(t, 0u, drow, st);
+        pack_store<CF, BULK>(t, 0u, drow, st);
     } else {
         // ---- butterfly partner in lane lg ^ (1 << li) ----------------------
         constexpr int li = P - CF::LB;
@@ -479,62 +407,14 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             if (fma_out<CF>(k)) t[k] = imad(mR, neg1, imad(own, one, PCo[a]));
             else t[k] = sub_add(own, mR, PCo[a]);
         }
-        pack_store<CF>(t, 0u - lb, drow, st);
-    }
-}
-
-// One trellis stage WITHOUT decisions (Eq. 1's min only): the stages below
-// the first survivor row any traceback reads (s < t0r + v, the truncated
-// block's warm-up) need the path metrics but no survivor bits, so the
-// decision operand, its packing and the store are skipped -- 2 instructions
-// per output register instead of ~4.4.
-template <class CF, int P>
-__device__ __forceinline__ void acs_stage_nodec(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
-                                                int lg) {
-    using C = typename CF::code;
-    constexpr int S = CF::S, NC = CF::NC;
-    constexpr int g0 = C::g0, gK = C::gK;
-    if constexpr (P < CF::LB) {
-        uint32_t Pv[NC];
-        bm_vector<CF, CF::lane_possible(P)>(xy, flip, Pv);
-        constexpr int pb = 1 << P;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            if (k & pb) continue;
-            const int a = CF::alpha_reg(k, P);
-            const uint32_t E = pm[k], O = pm[k | pb];
-            pm[k] = __viaddmin_s16x2(E, Pv[a], add32(O, Pv[a ^ g0]));             // Eqs. 3, 5
-            pm[k | pb] = __viaddmin_s16x2(E, Pv[a ^ gK], add32(O, Pv[a ^ gK ^ g0]));  // Eqs. 4, 6
-        }
-    } else {
-        constexpr int li = P - CF::LB;
-        const uint32_t lb = uint32_t(lg >> li) & 1u;
-        uint32_t recv[S];
-#pragma unroll
-        for (int k = 0; k < S; ++k) recv[k] = __shfl_xor_sync(0xffffffffu, pm[k], 1 << li);
-        uint32_t Po[NC], Pr[NC];
-        if constexpr (C::symmetric) {
-            bm_vector<CF, CF::lane_possible(P)>(xy, flip, Po);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) Pr[c] = Po[c ^ C::ALL];
-        } else {
-            const int fo = flip ^ (lb ? (gK ^ g0) : 0);
-            const int fr = flip ^ (lb ? gK : g0);
-            bm_vector<CF, CF::lane_possible(P) | (gK ^ g0)>(xy, fo, Po);
-            bm_vector<CF, CF::lane_possible(P) | gK | g0>(xy, fr, Pr);
-        }
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            const int a = CF::alpha_reg(k, P);
-            pm[k] = __viaddmin_s16x2(pm[k], Po[a], add32(recv[k], Pr[a]));
-        }
+        pack_store<CF, BULK>(t, 0u - lb, drow, st);
     }
 }
 
 // v stages at phases P..v-1, the operands of stage P+1 loaded one stage ahead
 // (one basic block: the scheduler overlaps stage P+1's loads and branch
 // metrics with stage P's butterflies).
-template <class CF, int P, bool FULL, bool DEC = true>
+template <class CF, int P, bool FULL, bool BULK = false>
 struct Cycle {
     static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const SoftSrc<CF>& src,
                                                const int (&flip)[CF::V], int lg, uint32_t* drow,
@@ -545,15 +425,14 @@ struct Cycle {
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst) nxt = src.load(s0 + P + 1);
             }
-            if constexpr (DEC)
-                acs_stage<CF, P>(pm, cur, flip[P], lg, drow + size_t(s0 + P) * CF::ROW,
-                                 !PBVD_SKIP_ROWS || s0 + P >= st_lo, one, neg1);
-            else
-                acs_stage_nodec<CF, P>(pm, cur, flip[P], lg);
+            // drow: this cycle's first survivor row (stage s0), so each
+            // stage's store address is a compile-time offset from it
+            acs_stage<CF, P, BULK>(pm, cur, flip[P], lg, drow + P * CF::ROW, s0 + P >= st_lo,
+                                   one, neg1);
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst)
-                    Cycle<CF, P + 1, FULL, DEC>::run(pm, src, flip, lg, drow, s0, nst, st_lo, nxt,
-                                                     one, neg1);
+                    Cycle<CF, P + 1, FULL, BULK>::run(pm, src, flip, lg, drow, s0, nst, st_lo, nxt,
+                                                      one, neg1);
             }
         }
     }
@@ -590,6 +469,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [2][PPW][LSTR]
     uint8_t* dep = wbase + CF::WRAW + CF::WLAM;                             // [BPW][RAWB]
     uint8_t* woffs = dep + CF::WDEP;                                        // [2][BPW]
+    uint32_t* stg = reinterpret_cast<uint32_t*>(wbase + CF::WSMEM - CF::WSTG); // [NSTG][V][ROW]
 
     // warp unit: interior warps first (BPW consecutive interior blocks), then
     // one unit per edge block (all lane groups replicate that block)
@@ -626,10 +506,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     // 16-byte cp.async of chunk c's soft windows: lane i copies block i's
     // window (rounded out to 16-byte vectors) to raw[c & 1][i]
     auto issue_raw = [&](int c) {
-#ifdef PBVD_EXP_NO_INPUT
-        cp_async_commit();
-        return;
-#endif
         const int s0 = c * T;
         const int nst = min(T, span - s0);
         uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
@@ -641,16 +517,9 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             woffs[(c & 1) * BPW + i] = uint8_t((vlo + uintptr_t(k0)) & 15);
             if (ga >= vlo && ga + RAWB <= vhi) {
                 // interior fast path: a fixed number of 16-byte vectors
-#if PBVD_IN_HINT
-                const uint64_t ipol = policy_evict_first_nv();
-#pragma unroll
-                for (int j = 0; j < RAWB / 16; ++j)
-                    cp_async16_hint(smem_u32(dst + 16 * j), reinterpret_cast<const void*>(ga + 16 * j), ipol);
-#else
 #pragma unroll
                 for (int j = 0; j < RAWB / 16; ++j)
                     cp_async16(smem_u32(dst + 16 * j), reinterpret_cast<const void*>(ga + 16 * j));
-#endif
             } else {
                 const int64_t k1 = kept_before(p, a + max(nst, 0), R) - p.kb_ws0;
                 const uintptr_t gb = (vlo + uintptr_t(k1) + 15) & ~uintptr_t(15);
@@ -679,7 +548,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         const int s0 = c * T;
         const int nst = min(T, span - s0);
         const uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
-#if PBVD_DEP_TABLE
         // table-driven: every dense word is one funnel-shifted window word
         // PRMT-ed with the (phase, word) selector of the host table -- all
         // words independent (no serial kept-index chain)
@@ -698,29 +566,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                 const uint32_t x = __funnelshift_r(win[q >> 2], win[(q >> 2) + 1], uint32_t(q & 3) * 8u);
                 dst[w] = prmt(x, 0u, e & 0xffffu);
             }
-        }
-        return;
-#endif
-        for (int i = lane; i < nblk; i += 32) {
-            const int64_t a = block_lo(i) + s0;
-            const uint8_t* src = rb + size_t(CF::wslot(i)) * RAWB + win_off(i, a);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(CF::wslot(i)) * RAWB);
-            int ph = int(((a % p.P) + p.P) % p.P), idx = 0, nb = 0;
-            uint32_t acc = 0;
-            for (int st = 0; st < nst; ++st) {
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const bool keep = (p.keep >> (r * p.P + ph)) & 1;
-                    const uint32_t val = keep ? uint32_t(src[idx++]) : 0u;
-                    acc |= val << (8 * (nb & 3));
-                    if ((++nb & 3) == 0) {
-                        dst[(nb >> 2) - 1] = acc;
-                        acc = 0;
-                    }
-                }
-                ph = (ph + 1 == p.P) ? 0 : ph + 1;
-            }
-            if (nb & 3) dst[nb >> 2] = acc;
         }
     };
     // Transform of chunk c, slice j of NCYC: the soft bytes of every (pair,
@@ -840,6 +685,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             __syncwarp();
         }
     }
+    int gcyc = 0;                 // cycles run so far (PBVD_BULK_STORE slot index)
     for (int c = 0; c < nchunks; ++c) {
         const int nst = min(T, span - c * T);
         const bool next = c + 1 < nchunks;
@@ -873,35 +719,36 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             // (within a cycle Cycle<> loads one stage ahead); the read past the
             // chunk's last stage stays inside the operand row's padding
             XY<CF> first = src.load(0);
-            // cycles wholly below the first survivor row the traceback reads:
-            // path metrics only (acs_stage_nodec)
-            const int jd = PBVD_NODEC_WARMUP ? min(ncyc, max(0, st_lo / V)) : 0;
 #pragma unroll 1
-            for (int j = 0; j < jd; ++j) {
+            for (int j = 0; j < ncyc; ++j) {
                 const int s0 = j * V;
                 const XY<CF> nfirst = src.load(s0 + V);
-                Cycle<CF, 0, true, false>::run(pm, src, flip, lg, drow, s0, T, st_lo, first, p.one,
-                                               p.neg_one);
+                if constexpr (PBVD_BULK_STORE) {
+                    // stage the cycle's survivor rows in shared-memory slot
+                    // gcyc % NSTG, then one bulk copy to the region
+                    const int slot = gcyc % CF::NSTG;
+                    if (lane == 0) bulk_wait_read<CF::NSTG - 1>();    // the slot's last copy has read it
+                    __syncwarp();
+                    uint32_t* srow = stg + size_t(slot) * V * ROW;
+                    Cycle<CF, 0, true, true>::run(pm, src, flip, lg, srow + size_t(lane) * CF::WPS,
+                                                  s0, T, st_lo, first, p.one, p.neg_one);
+                    __syncwarp();
+                    if (lane == 0 && s0 + V > st_lo) {
+                        fence_proxy_async_smem();
+                        bulk_s2g(gdec + (size_t(c) * T + s0) * ROW, smem_u32(srow), uint32_t(V * ROW * 4));
+                        bulk_commit();
+                    }
+                    ++gcyc;
+                } else {
+                    Cycle<CF, 0, true>::run(pm, src, flip, lg, drow + size_t(s0) * ROW, s0, T, st_lo,
+                                            first, p.one, p.neg_one);
+                }
                 first = nfirst;
-                transform(c + 1, j);
-            }
-#pragma unroll 1
-            for (int j = jd; j < ncyc; ++j) {
-                const int s0 = j * V;
-#if PBVD_CYCLE_PREFETCH
-                const XY<CF> nfirst = src.load(s0 + V);
-                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, T, st_lo, first, p.one,
-                                        p.neg_one);
-                first = nfirst;
-#else
-                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow, s0, T, st_lo, src.load(s0),
-                                        p.one, p.neg_one);
-#endif
                 transform(c + 1, j);     // harmless past the last chunk
             }
         }
         if (ncyc * V < nst)   // (the last chunk of an edge block)
-            Cycle<CF, 0, false>::run(pm, src, flip, lg, drow, ncyc * V, nst, st_lo,
+            Cycle<CF, 0, false>::run(pm, src, flip, lg, drow + size_t(ncyc * V) * ROW, ncyc * V, nst, st_lo,
                                      src.load(ncyc * V), p.one, p.neg_one);
         // renormalise: subtract the block minimum (per 16-bit half = per block)
         uint32_t mn = pm[0];
@@ -914,6 +761,10 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         __syncwarp();      // every lane is done with lam[c & 1] before chunk c+2's transform
     }
 
+    if constexpr (PBVD_BULK_STORE) {
+        if (lane == 0) bulk_wait<0>();    // every survivor row is in global memory
+        __syncwarp();
+    }
     // ---- traceback start: min PM, lowest logical state on ties --------
     const int pend = span % V;
     // key = (PM << SB) | logical state: SB = max(8, v) bits of state (16 + 11 <= 32)
@@ -956,9 +807,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         const int nblk_tb = edge ? 1 : int(min(int64_t(BPW), int64_t(p.n_int) - wb0));
 #ifdef PBVD_EXP_TIMING
         if (p.dbg && lane == 0) p.dbg[8 * gw + 1] = gtime();
-#endif
-#ifdef PBVD_EXP_NO_TB
-        if (nblk_tb > 0) return;     // timing experiment only: skip the walk
 #endif
         warp_traceback<CF>(wbase, gdec, span, edge ? p.edges[e].t0r : p.t0r,
                            edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,

@@ -60,7 +60,6 @@ struct FwdParams {
     uint32_t one, neg_one; // 1 and 0xffffffff, opaque to the compiler (pipe balancing)
     int P;                 // puncture period (1 = none)
     int kp;                // kept values per period
-    uint64_t keep;         // keep flag of (r, p) at bit r*P + p
     int cum[16];           // kept values in columns [0, p) of one period
     // depuncture table (P > 1): entry [ph0][w] for dense word w of a chunk
     // starting at phase ph0 -- bits 0-15 a PRMT selector over the 4 kept

@@ -306,7 +306,6 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
     fp.neg_one = 0xffffffffu;
     fp.P = h->P;
     fp.kp = h->kp;
-    fp.keep = h->keep;
     fp.dtab = h->dtab;
     for (int i = 0; i < 16; ++i) fp.cum[i] = h->cum[i];
     fp.dec = dec_int;

@@ -333,14 +333,8 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
             const uint32_t mb = smem_u32(&mbar[k % NBUF]);
             const int c = c_top - k;
             mbar_arrive_expect_tx(mb, bytes);
-#if PBVD_L2_HINTS
-            bulk_g2s_hint(smem_u32(ring + ((size_t(k % NBUF) * NR + tid) * TT + (lo - c * TT)) * ROW),
-                          rbase + size_t(tid) * rstride + size_t(lo) * ROW, bytes, mb,
-                          policy_evict_first());
-#else
             bulk_g2s(smem_u32(ring + ((size_t(k % NBUF) * NR + tid) * TT + (lo - c * TT)) * ROW),
                      rbase + size_t(tid) * rstride + size_t(lo) * ROW, bytes, mb);
-#endif
         }
     };
     auto wait = [&](int k) { mbar_wait(smem_u32(&mbar[k % NBUF]), uint32_t(k / NBUF) & 1u); };
@@ -467,14 +461,8 @@ __global__ void __launch_bounds__(128) tb_kernel(const __grid_constant__ TbParam
 // L2; while one warp walks (latency bound), the other warps of its SM
 // sub-partition keep the ALU pipes busy with their forward passes, and the
 // second launch and its grid-wide dependency disappear.
-#ifndef PBVD_TB_PREFETCH
-#define PBVD_TB_PREFETCH 0
-#endif
 #ifndef PBVD_FUSED_TT
 #define PBVD_FUSED_TT 18
-#endif
-#ifndef PBVD_TB_DISCARD
-#define PBVD_TB_DISCARD 0
 #endif
 #ifndef PBVD_FUSED_NBUF
 #define PBVD_FUSED_NBUF 3
@@ -536,18 +524,6 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
     auto wait = [&](int k) { mbar_wait(smem_u32(&mbar[k % NBUF]), uint32_t(k / NBUF) & 1u); };
 
     for (int k = 0; k < min(NBUF - 1, nchunks); ++k) issue(k);
-#if PBVD_TB_PREFETCH
-    // every later chunk of the region goes in flight to L2 at once, so the
-    // ring's bulk copies hit L2 instead of waiting on HBM one chunk at a time
-    if (lane == 0) {
-        for (int k = NBUF - 1; k < nchunks; ++k) {
-            int lo, hi;
-            chunk_rows(k, lo, hi);
-            bulk_prefetch_l2(region + size_t(lo) * ROW, uint32_t(hi - lo) * ROW * 4u);
-        }
-    }
-#endif
-
     const int pe = span % V;
     const int nbits = t1r - t0r;
     const int nwords = (nbits + 31) >> 5;
@@ -646,15 +622,6 @@ __device__ __forceinline__ void warp_traceback(uint8_t* wsm, const uint32_t* reg
 #ifdef PBVD_EXP_TIMING
             cc += clock64() - c1;
             if (dbg && lane == 0 && k == nchunks - 1) { dbg[4] = cw; dbg[5] = cc; dbg[6] = nchunks; }
-#endif
-#if PBVD_TB_DISCARD
-            // the chunk's survivor rows are dead now: drop their L2 lines
-            // without a write-back (they were read into the ring already)
-            {
-                const uint8_t* g0 = reinterpret_cast<const uint8_t*>(region + size_t(lo) * ROW);
-                const int nl = (hi - lo) * ROW * 4 / 128;
-                for (int i = lane; i < nl; i += 32) discard_l2_line(g0 + size_t(i) * 128);
-            }
 #endif
             __syncwarp();          // slot k % NBUF free for chunk k + NBUF
         }
