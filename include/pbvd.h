@@ -105,20 +105,37 @@ int pbvd_create(pbvd_t *out, int K, int R, const uint32_t *polys, int punct_peri
                 const uint8_t *punct, int D, int L, int soft_bits, unsigned flags,
                 int device);
 
+/* Release the handle, its device tables and survivor workspace (and any host
+ * pipeline streams).  h may be NULL.  The caller must have finished (or
+ * synchronised) every decode issued on h and closed its pbvd_stream_t objects;
+ * the caller's buffers are not touched.  No error is reported. */
 void pbvd_destroy(pbvd_t h);
 
-/* Number of int8 soft values of a stream with n_info info bits (including the
- * K-1 tail stages if TERMINATED, after puncturing).  Negative on error. */
+/* Number of int8 soft values of a stream with n_info info bits: R per stage
+ * (one per coded bit, Eq. 2) over n_info stages plus the K-1 zero
+ * tail stages if TERMINATED (reading c-13), minus the punctured positions
+ * (reading c-18: column s mod P of the keep matrix).  PBVD_EINVAL for a NULL
+ * handle or n_info < 1 (message in pbvd_last_error(h)). */
 int64_t pbvd_llr_count(pbvd_t h, int64_t n_info);
 
-/* Number of stages (n_info, plus K-1 if TERMINATED) and blocks ceil(n_info/D). */
+/* Number of trellis stages (n_info, plus K-1 if TERMINATED) and of blocks
+ * ceil(n_info/D) (the decoding blocks of P:93; the last one may hold
+ * fewer than D bits, reading c-22).  PBVD_EINVAL as pbvd_llr_count. */
 int64_t pbvd_stage_count(pbvd_t h, int64_t n_info);
 int64_t pbvd_block_count(pbvd_t h, int64_t n_info);
 
-/* Decode a whole stream.
- *   d_llr  device, n_llr == pbvd_llr_count(n_info) int8 values
+/* Decode a whole stream: the PBVD of §III.A -- every
+ * block's forward ACS over its parallel block [bD-L, bD+D+L) (Eq. 1, P:72-74;
+ * branch metrics from the 2^R codeword metrics, Eqs. 3-6), survivor decisions
+ * (P:258), traceback from the min-PM state (state 0 with
+ * PBVD_START_ZERO) through the L traceback stages, D bits emitted per
+ * block (Alg. 1 K2), packed LSB-first.
+ *   d_llr  device, n_llr == pbvd_llr_count(n_info) int8 values, [stage][r]
  *   d_bits device, >= ceil(n_info/8) bytes, fully written (pad bits 0)
- * Asynchronous on `stream`. */
+ *   stream cudaStream_t (NULL = legacy default stream)
+ * Errors: PBVD_EINVAL (NULL pointer, n_info < 1), PBVD_ESIZE (n_llr differs
+ * from pbvd_llr_count), PBVD_ENOMEM (workspace), PBVD_ECUDA (launch); the
+ * message is in pbvd_last_error(h).  Asynchronous on `stream`. */
 int pbvd_decode(pbvd_t h, const int8_t *d_llr, int64_t n_llr, uint8_t *d_bits, int64_t n_info,
                 void *stream);
 

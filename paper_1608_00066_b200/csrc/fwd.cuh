@@ -58,11 +58,6 @@
 #ifndef PBVD_MAXREG_S64
 #define PBVD_MAXREG_S64 200
 #endif
-// survivor rows staged in shared memory and written by cp.async.bulk (one
-// bulk copy per v-stage cycle) instead of direct 8-byte stores per lane
-#ifndef PBVD_BULK_STORE
-#define PBVD_BULK_STORE 0
-#endif
 
 namespace pbvd {
 
@@ -139,10 +134,7 @@ struct Cfg {
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
     static constexpr size_t WLAM = size_t(2) * PPW * LSTR * 4;   // double buffered
     static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
-    // PBVD_BULK_STORE: NSTG slots of one v-stage cycle of survivor rows
-    static constexpr int NSTG = 4;
-    static constexpr size_t WSTG = PBVD_BULK_STORE ? size_t(NSTG) * V * ROW * 4 : 0;
-    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128 + WSTG;
+    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
 
     // alpha of the butterfly whose E slot has register index k, restricted
@@ -240,7 +232,7 @@ __device__ __forceinline__ void bm_vector(const XY<CF>& xy, int flip, uint32_t (
 // store them to this lane's shared-memory row.  Bit layout of word kw:
 // slot q_reg = 16*kw + (b & 15) of block half (b >> 4)   (S >= 16), or
 // bit = 16*h + 8*(q_reg / (S/2)) + q_reg % (S/2)         (S < 16).
-template <class CF, bool BULK = false>
+template <class CF>
 __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t inv,
                                            uint32_t* drow, bool st) {
     constexpr int S = CF::S, WPS = CF::WPS;
@@ -272,20 +264,6 @@ __device__ __forceinline__ void pack_store(const uint32_t (&t)[CF::S], uint32_t 
         }
         words[0] = (wd ^ inv) & (0x01010101u * ((1u << H) - 1u));
     }
-    if constexpr (BULK) {
-        // drow: this lane's words of the row in the shared-memory staging slot
-        if constexpr (WPS == 1) {
-            drow[0] = words[0];
-        } else if constexpr (WPS == 2) {
-            *reinterpret_cast<uint2*>(drow) = make_uint2(words[0], words[1]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < WPS; i += 4)
-                *reinterpret_cast<uint4*>(drow + i) =
-                    make_uint4(words[i], words[i + 1], words[i + 2], words[i + 3]);
-        }
-        return;
-    }
     if (!st) return;       // a row the traceback never reads (below its first row)
     // survivor stores with an L2 eviction-priority hint (the fused traceback
     // re-reads them from L2)
@@ -312,7 +290,7 @@ __host__ __device__ constexpr bool fma_out(int k) {
     return (k & 1) != 0;
 }
 
-template <class CF, int P, bool BULK = false>
+template <class CF, int P>
 __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& xy, int flip,
                                           int lg, uint32_t* drow, bool st, uint32_t one,
                                           uint32_t neg1) {
@@ -352,7 +330,7 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             t[k] = add32(d, KC[a]);
             t[k | pb] = add32(d, KC[a ^ gK]);
         }
-        pack_store<CF, BULK>(t, 0u, drow, st);
+        pack_store<CF>(t, 0u, drow, st);
         return;
         }
 #pragma unroll
@@ -375,7 +353,7 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             t[k] = tE;
             t[k | pb] = tO;
         }
-        pack_store<CF, BULK>(t, 0u, drow, st);
+        pack_store<CF>(t, 0u, drow, st);
     } else {
         // ---- butterfly partner in lane lg ^ (1 << li) ----------------------
         constexpr int li = P - CF::LB;
@@ -407,18 +385,18 @@ __device__ __forceinline__ void acs_stage(uint32_t (&pm)[CF::S], const XY<CF>& x
             if (fma_out<CF>(k)) t[k] = imad(mR, neg1, imad(own, one, PCo[a]));
             else t[k] = sub_add(own, mR, PCo[a]);
         }
-        pack_store<CF, BULK>(t, 0u - lb, drow, st);
+        pack_store<CF>(t, 0u - lb, drow, st);
     }
 }
 
 // v stages at phases P..v-1, the operands of stage P+1 loaded one stage ahead
 // (one basic block: the scheduler overlaps stage P+1's loads and branch
 // metrics with stage P's butterflies).
-template <class CF, int P, bool FULL, bool BULK = false>
+template <class CF, int P, bool FULL>
 struct Cycle {
     static __device__ __forceinline__ void run(uint32_t (&pm)[CF::S], const SoftSrc<CF>& src,
                                                const int (&flip)[CF::V], int lg, uint32_t* drow,
-                                               int s0, int nst, int st_lo, const XY<CF>& cur,
+                                               int s0, int nst, bool st, const XY<CF>& cur,
                                                uint32_t one, uint32_t neg1) {
         if constexpr (P < CF::V) {
             XY<CF> nxt = cur;
@@ -427,12 +405,11 @@ struct Cycle {
             }
             // drow: this cycle's first survivor row (stage s0), so each
             // stage's store address is a compile-time offset from it
-            acs_stage<CF, P, BULK>(pm, cur, flip[P], lg, drow + P * CF::ROW, s0 + P >= st_lo,
-                                   one, neg1);
+            acs_stage<CF, P>(pm, cur, flip[P], lg, drow + P * CF::ROW, st, one, neg1);
             if constexpr (P + 1 < CF::V) {
                 if (FULL || s0 + P + 1 < nst)
-                    Cycle<CF, P + 1, FULL, BULK>::run(pm, src, flip, lg, drow, s0, nst, st_lo, nxt,
-                                                      one, neg1);
+                    Cycle<CF, P + 1, FULL>::run(pm, src, flip, lg, drow, s0, nst, st, nxt, one,
+                                                neg1);
             }
         }
     }
@@ -469,7 +446,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [2][PPW][LSTR]
     uint8_t* dep = wbase + CF::WRAW + CF::WLAM;                             // [BPW][RAWB]
     uint8_t* woffs = dep + CF::WDEP;                                        // [2][BPW]
-    uint32_t* stg = reinterpret_cast<uint32_t*>(wbase + CF::WSMEM - CF::WSTG); // [NSTG][V][ROW]
 
     // warp unit: interior warps first (BPW consecutive interior blocks), then
     // one unit per edge block (all lane groups replicate that block)
@@ -685,7 +661,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             __syncwarp();
         }
     }
-    int gcyc = 0;                 // cycles run so far (PBVD_BULK_STORE slot index)
     for (int c = 0; c < nchunks; ++c) {
         const int nst = min(T, span - c * T);
         const bool next = c + 1 < nchunks;
@@ -709,7 +684,9 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         // survivor rows of this chunk, this lane's WPS words (direct stores:
         // each warp writes 32 * WPS contiguous words per stage)
         uint32_t* drow = gdec + size_t(c) * T * ROW + size_t(lane) * CF::WPS;
-        const int st_lo = s_read - c * T;     // rows below the traceback's first row: no store
+        // cycles wholly below the traceback's first row store no survivors
+        // (one predicate per cycle: the rows of a straddling cycle are stored)
+        const int st_lo = s_read - c * T;
         // whole v-stage cycles of the chunk run in the one hot loop (interior
         // spans are padded to a multiple of v); only an edge block's last
         // chunk can leave a remainder of < v stages
@@ -723,32 +700,14 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             for (int j = 0; j < ncyc; ++j) {
                 const int s0 = j * V;
                 const XY<CF> nfirst = src.load(s0 + V);
-                if constexpr (PBVD_BULK_STORE) {
-                    // stage the cycle's survivor rows in shared-memory slot
-                    // gcyc % NSTG, then one bulk copy to the region
-                    const int slot = gcyc % CF::NSTG;
-                    if (lane == 0) bulk_wait_read<CF::NSTG - 1>();    // the slot's last copy has read it
-                    __syncwarp();
-                    uint32_t* srow = stg + size_t(slot) * V * ROW;
-                    Cycle<CF, 0, true, true>::run(pm, src, flip, lg, srow + size_t(lane) * CF::WPS,
-                                                  s0, T, st_lo, first, p.one, p.neg_one);
-                    __syncwarp();
-                    if (lane == 0 && s0 + V > st_lo) {
-                        fence_proxy_async_smem();
-                        bulk_s2g(gdec + (size_t(c) * T + s0) * ROW, smem_u32(srow), uint32_t(V * ROW * 4));
-                        bulk_commit();
-                    }
-                    ++gcyc;
-                } else {
-                    Cycle<CF, 0, true>::run(pm, src, flip, lg, drow + size_t(s0) * ROW, s0, T, st_lo,
-                                            first, p.one, p.neg_one);
-                }
+                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow + size_t(s0) * ROW, s0, T, s0 + V > st_lo,
+                                        first, p.one, p.neg_one);
                 first = nfirst;
                 transform(c + 1, j);     // harmless past the last chunk
             }
         }
         if (ncyc * V < nst)   // (the last chunk of an edge block)
-            Cycle<CF, 0, false>::run(pm, src, flip, lg, drow + size_t(ncyc * V) * ROW, ncyc * V, nst, st_lo,
+            Cycle<CF, 0, false>::run(pm, src, flip, lg, drow + size_t(ncyc * V) * ROW, ncyc * V, nst, true,
                                      src.load(ncyc * V), p.one, p.neg_one);
         // renormalise: subtract the block minimum (per 16-bit half = per block)
         uint32_t mn = pm[0];
@@ -761,10 +720,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         __syncwarp();      // every lane is done with lam[c & 1] before chunk c+2's transform
     }
 
-    if constexpr (PBVD_BULK_STORE) {
-        if (lane == 0) bulk_wait<0>();    // every survivor row is in global memory
-        __syncwarp();
-    }
     // ---- traceback start: min PM, lowest logical state on ties --------
     const int pend = span % V;
     // key = (PM << SB) | logical state: SB = max(8, v) bits of state (16 + 11 <= 32)

@@ -8,6 +8,5 @@ void add_variants_k9(std::vector<Variant>& v) {
     // two-kernel path (pbvd_set_fused(h, 0)) -- see DESIGN.md section 7
     v.push_back(make_variant<C9, 4>(0));
     v.push_back(make_variant<C9, 8>(1));
-    v.push_back(make_variant<C9, 16>(2));
 }
 }  // namespace pbvd

@@ -50,10 +50,6 @@ __device__ __forceinline__ uint32_t add32(uint32_t a, uint32_t b) {
 __device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
 }
-__device__ __forceinline__ void cp_async16_hint(uint32_t sdst, const void* gsrc, uint64_t pol) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-                 ::"r"(sdst), "l"(gsrc), "l"(pol) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -62,39 +58,14 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// ---- bulk (TMA engine, non-tensor) copies ---------------------------------
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 // generic-proxy accesses (global and shared) before later async-proxy ones
 __device__ __forceinline__ void fence_proxy_async_all() {
     asm volatile("fence.proxy.async;" ::: "memory");
-}
-// shared::cta -> global, completion tracked by bulk async-groups
-__device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                 ::"l"(gdst), "r"(ssrc), "r"(bytes) : "memory");
-}
-// the same with an L2 cache-policy hint (createpolicy)
-__device__ __forceinline__ void bulk_s2g_hint(void* gdst, uint32_t ssrc, uint32_t bytes,
-                                              uint64_t policy) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
-                 ::"l"(gdst), "r"(ssrc), "r"(bytes), "l"(policy) : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
 }
 // non-volatile variants: the compiler may hoist / share them
 __device__ __forceinline__ uint64_t policy_evict_last_nv() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_first_nv() {
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ void st_global_v2_hint(void* p, uint32_t a, uint32_t b, uint64_t pol) {
@@ -109,37 +80,6 @@ __device__ __forceinline__ void st_global_v4_hint(void* p, uint32_t a, uint32_t 
 __device__ __forceinline__ void st_global_hint(void* p, uint32_t a, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(pol) : "memory");
 }
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void bulk_g2s_hint(uint32_t sdst, const void* gsrc, uint32_t bytes,
-                                              uint32_t mbar, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], %4;"
-        ::"r"(sdst), "l"(gsrc), "r"(bytes), "r"(mbar), "l"(policy) : "memory");
-}
-// invalidate one 128-byte L2 line without writing it back (dead data)
-__device__ __forceinline__ void discard_l2_line(const void* g) {
-    asm volatile("discard.global.L2 [%0], 128;" ::"l"(g) : "memory");
-}
-// L2 prefetch of a global range (no completion tracking)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
 // global -> shared::cta (shared::cluster address of own CTA), mbarrier tx
 __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* gsrc, uint32_t bytes,
                                          uint32_t mbar) {
@@ -148,17 +88,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* gsrc, uint32
         ::"r"(sdst), "l"(gsrc), "r"(bytes), "r"(mbar) : "memory");
 }
 
-// TMA tensor load of one box row of box[0] elements starting at column x
-// (any integer, no alignment; out-of-range elements are zero-filled) of a
-// 2-D [1][n] tensor map
-__device__ __forceinline__ void tma_load_row(uint32_t sdst, const void* tmap, int32_t x,
-                                             uint32_t mbar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3}], [%4];"
-        ::"r"(sdst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(0), "r"(mbar)
-        : "memory");
-}
 
 // ---- programmatic dependent launch ------------------------------------------
 __device__ __forceinline__ void pdl_launch_dependents() {
@@ -178,9 +107,6 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t mbar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  ::"r"(mbar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
     asm volatile(
