@@ -63,10 +63,10 @@ def parse():
 def eq8_model(D, L, nblocks, U1, B, S_k, n_streams=3):
     """The paper's Eq. 8 throughput model and its transfer-bound
     counterpart for this pipeline (paper_1608_00066_b200/model.py), with the
-    segmentation pbvd_decode_host uses (nseg = min(2 n_streams, nblocks/8192),
+    segmentation pbvd_decode_host uses (nseg = min(4 n_streams, nblocks/4096),
     pbvd.cu), the measured H2D rate B and S_k = the device-timed value."""
     from paper_1608_00066_b200 import model as M
-    nseg = max(1, min(2 * n_streams, nblocks // 8192))
+    nseg = max(1, min(4 * n_streams, nblocks // 4096))
     seg = -(-nblocks // nseg)
     nseg = -(-nblocks // seg)
     out = M.model(D, L, seg, nseg, U1, 1 / 8, B, S_k)

@@ -52,6 +52,8 @@ struct HostLane {
     size_t llr_cap = 0;
     uint8_t* d_bits = nullptr;
     size_t bits_cap = 0;
+    cudaEvent_t in_ready = nullptr;   // this lane's staging buffer holds its segment
+    cudaEvent_t consumed = nullptr;   // its decode has read the staging buffer
 };
 
 struct pbvd_s {
@@ -74,6 +76,7 @@ struct pbvd_s {
     Workspace ws;
     size_t ws_limit = size_t(4) << 30;
     std::vector<HostLane> lanes;
+    cudaStream_t h2d = nullptr;        // host pipeline: every H2D copy, in stream order
     bool prof = false;
     bool fused = true;     // forward + in-warp traceback in one kernel (pbvd_set_fused)
     int n_mirror = 0;      // extra output destinations of the current call (byte offsets)
@@ -642,8 +645,11 @@ void pbvd_destroy(pbvd_t h) {
             if (ln.d_llr) cudaFree(ln.d_llr);
             if (ln.d_bits) cudaFree(ln.d_bits);
             if (ln.stream) cudaStreamDestroy(ln.stream);
+            if (ln.in_ready) cudaEventDestroy(ln.in_ready);
+            if (ln.consumed) cudaEventDestroy(ln.consumed);
         }
         for (auto ev : h->ev_pool) cudaEventDestroy(ev);
+        if (h->h2d) cudaStreamDestroy(h->h2d);
     }
     delete h;
 }
@@ -730,23 +736,50 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
     const Variant* var_saved = h->var;
     h->var = h->host_var;
     const int64_t kb0 = kept_before_h(h, window_stage0);
-    // segments: enough of them to overlap copies with kernels, each large
-    // enough to keep the GPU busy on its own
-    const int64_t min_seg = 8192;
-    int64_t nseg = std::max<int64_t>(1, std::min<int64_t>(2 * n_streams, nblocks / min_seg));
+    // Pipeline (§IV.C, B200 form): every H2D copy goes through ONE
+    // stream, in order, so each runs at the full link rate (copies on several
+    // streams run concurrently on several copy engines and only share the
+    // link); segment k's decode (and its D2H) runs on lane k % n_streams as
+    // soon as its copy has landed, while later copies continue.  A lane's
+    // staging buffer is refilled only after its previous decode has read it.
+    // The stream is PCIe-bound, so what is left after the last H2D byte is
+    // one segment's decode latency plus its D2H.
+    const int64_t min_seg = 4096;
+    int64_t nseg = std::max<int64_t>(1, std::min<int64_t>(4 * n_streams, nblocks / min_seg));
     const int64_t seg = (nblocks + nseg - 1) / nseg;
     nseg = (nblocks + seg - 1) / seg;
+    if (!h->h2d && cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) != cudaSuccess) {
+        h->prof = prof;
+        h->var = var_saved;
+        return cuda_fail(h, cudaGetLastError(), "cudaStreamCreate");
+    }
     while (int(h->lanes.size()) < n_streams) {
         HostLane ln;
-        if (cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking) != cudaSuccess) {
+        if (cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ln.in_ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ln.consumed, cudaEventDisableTiming) != cudaSuccess) {
             h->prof = prof;
             h->var = var_saved;
-            return cuda_fail(h, cudaGetLastError(), "cudaStreamCreate");
+            return cuda_fail(h, cudaGetLastError(), "cudaStreamCreate / cudaEventCreate");
         }
         h->lanes.push_back(ln);
     }
     int rc = PBVD_OK;
     const int64_t bit_base = block0 * h->D;
+    // staging buffers sized for the largest segment, before any copy is queued
+    for (int i = 0; i < n_streams && rc == PBVD_OK; ++i) {
+        HostLane& ln = h->lanes[size_t(i)];
+        const BlockGeo ga = geo(h, n_info_total, n_stages, nb, block0);
+        const BlockGeo gz = geo(h, n_info_total, n_stages, nb, std::min(block0 + nblocks, block0 + seg) - 1);
+        const int64_t span_max = (gz.hi - ga.lo) + 2 * (h->L + h->V) + h->D;
+        rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_llr), &ln.llr_cap,
+                        size_t(kept_before_h(h, span_max) + h->R * 16));
+        if (!rc) rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_bits), &ln.bits_cap,
+                                 size_t((seg * h->D + 7) / 8));
+        if (!rc) {
+            cudaEventRecord(ln.consumed, ln.stream);   // buffers free
+        }
+    }
     for (int64_t k = 0; k < nseg && rc == PBVD_OK; ++k) {
         HostLane& ln = h->lanes[size_t(k % n_streams)];
         const int64_t b0 = block0 + k * seg;
@@ -761,11 +794,18 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
         const size_t nllr = size_t(k1 - k0);
         const int64_t t0 = b0 * h->D, t1 = std::min<int64_t>(b1 * h->D, n_info_total);
         const size_t nbytes = size_t((t1 - t0 + 7) / 8);
-        rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_llr), &ln.llr_cap, nllr);
-        if (!rc) rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_bits), &ln.bits_cap, nbytes);
-        if (rc) break;
-        cudaError_t e = cudaMemcpyAsync(ln.d_llr, h_llr_window + (k0 - kb0), nllr,
-                                        cudaMemcpyHostToDevice, ln.stream);
+        if (nllr > ln.llr_cap || nbytes > ln.bits_cap) {
+            rc = fail(h, PBVD_ENOMEM, "host pipeline staging buffer too small");
+            break;
+        }
+        // H2D on the copy stream once the lane's previous decode has read
+        // the buffer
+        cudaError_t e = cudaStreamWaitEvent(h->h2d, ln.consumed, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(ln.d_llr, h_llr_window + (k0 - kb0), nllr, cudaMemcpyHostToDevice,
+                                h->h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(ln.in_ready, h->h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ln.stream, ln.in_ready, 0);
         if (e != cudaSuccess) {
             rc = cuda_fail(h, e, "cudaMemcpyAsync H2D");
             break;
@@ -773,9 +813,15 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
         rc = run_blocks(h, ln.ws, ln.d_llr, ga.lo, int64_t(nllr), n_info_total, b0, b1 - b0,
                         ln.d_bits, ln.stream);
         if (rc) break;
-        e = cudaMemcpyAsync(h_bits + (t0 - bit_base) / 8, ln.d_bits, nbytes,
-                            cudaMemcpyDeviceToHost, ln.stream);
+        e = cudaEventRecord(ln.consumed, ln.stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_bits + (t0 - bit_base) / 8, ln.d_bits, nbytes,
+                                cudaMemcpyDeviceToHost, ln.stream);
         if (e != cudaSuccess) rc = cuda_fail(h, e, "cudaMemcpyAsync D2H");
+    }
+    {
+        cudaError_t e = cudaStreamSynchronize(h->h2d);
+        if (!rc && e != cudaSuccess) rc = cuda_fail(h, e, "host pipeline H2D");
     }
     for (int i = 0; i < n_streams; ++i) {
         cudaError_t e = cudaStreamSynchronize(h->lanes[size_t(i)].stream);
