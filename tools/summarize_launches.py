@@ -13,7 +13,11 @@ def main(src, dst):
     for r in rows:
         name, val = r[4], float(r[14].replace(",", ""))
         if "fwd_kernel" in name:
-            key = "fwd_kernel<fused>" if ("ELb1E" in name or ", true>" in name or name.rstrip().endswith(", 1>(pbvd::FwdParams)")) else "fwd_kernel"
+            # template args <Cfg<...>, FUSED, MIRROR> (mangled, bool or int form)
+            tail = name.split(">, ")[-1] if ">, " in name else ""
+            fused = ("ELb1E" in name or ", true>" in name or "(bool)1" in name or
+                     tail.startswith("1,") or tail.startswith("true"))
+            key = "fwd_kernel<fused>" if fused else "fwd_kernel"
         elif "tb_kernel" in name:
             key = "tb_kernel"
         elif "acs_probe" in name:
