@@ -684,8 +684,11 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         // survivor rows of this chunk, this lane's WPS words (direct stores:
         // each warp writes 32 * WPS contiguous words per stage)
         uint32_t* drow = gdec + size_t(c) * T * ROW + size_t(lane) * CF::WPS;
-        // cycles wholly below the traceback's first row store no survivors
-        // (one predicate per cycle: the rows of a straddling cycle are stored)
+        uint32_t* const drow0 = gdec + size_t(lane) * CF::WPS;     // rows [0, v): never read
+        // cycles wholly below the traceback's first row (s_read >= v) write
+        // their survivor rows over the region's rows [0, v) instead -- rows
+        // no traceback reads, so those stores stay in L2 and never reach HBM
+        // (one select per cycle; a predicate per store cost 0.5 %)
         const int st_lo = s_read - c * T;
         // whole v-stage cycles of the chunk run in the one hot loop (interior
         // spans are padded to a multiple of v); only an edge block's last
@@ -700,8 +703,9 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             for (int j = 0; j < ncyc; ++j) {
                 const int s0 = j * V;
                 const XY<CF> nfirst = src.load(s0 + V);
-                Cycle<CF, 0, true>::run(pm, src, flip, lg, drow + size_t(s0) * ROW, s0, T, s0 + V > st_lo,
-                                        first, p.one, p.neg_one);
+                uint32_t* crow = (s0 + V > st_lo) ? drow + size_t(s0) * ROW : drow0;
+                Cycle<CF, 0, true>::run(pm, src, flip, lg, crow, s0, T, true, first, p.one,
+                                        p.neg_one);
                 first = nfirst;
                 transform(c + 1, j);     // harmless past the last chunk
             }
