@@ -63,10 +63,12 @@ def parse():
 def eq8_model(D, L, nblocks, U1, B, S_k, n_streams=3):
     """The paper's Eq. 8 throughput model and its transfer-bound
     counterpart for this pipeline (paper_1608_00066_b200/model.py), with the
-    segmentation pbvd_decode_host uses (nseg = min(4 n_streams, nblocks/4096),
-    pbvd.cu), the measured H2D rate B and S_k = the device-timed value."""
+    segmentation pbvd_decode_host uses (max(4, min(4 n_streams, nblocks/16384))
+    equal segments plus a 4096-block last one, pbvd.cu), the measured H2D rate B
+    and S_k = the device-timed value."""
     from paper_1608_00066_b200 import model as M
-    nseg = max(1, min(4 * n_streams, nblocks // 4096))
+    last = 4096 if nblocks >= 4 * 4096 else 0
+    nseg = max(4, min(4 * n_streams, (nblocks - last) // 16384)) + (1 if last else 0)
     seg = -(-nblocks // nseg)
     nseg = -(-nblocks // seg)
     out = M.model(D, L, seg, nseg, U1, 1 / 8, B, S_k)

@@ -744,10 +744,29 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
     // staging buffer is refilled only after its previous decode has read it.
     // The stream is PCIe-bound, so what is left after the last H2D byte is
     // one segment's decode latency plus its D2H.
-    const int64_t min_seg = 4096;
-    int64_t nseg = std::max<int64_t>(1, std::min<int64_t>(4 * n_streams, nblocks / min_seg));
-    const int64_t seg = (nblocks + nseg - 1) / nseg;
-    nseg = (nblocks + seg - 1) / seg;
+    // Segment plan: at least 4 and at most 4 per stream equal segments
+    // (>= 16384 blocks each beyond 4: every H2D copy costs a few us of setup,
+    // and a segment's decode must end before the next copy does), then a
+    // small last one (4096 blocks: one warp per sub-partition, so its decode
+    // -- all that is left after the last copy -- takes one lone warp's latency
+    // and its D2H is short).  Measured (tools/e2e_sweep.py): C4 +8 %, C3a +4 %
+    // e2e, C2 unchanged against 4 equal segments.  PBVD_HOST_NSEG /
+    // PBVD_HOST_LAST override the plan.
+    static const int64_t env_nseg = [] { const char* e = std::getenv("PBVD_HOST_NSEG"); return e ? std::atoll(e) : 0; }();
+    static const int64_t env_last = [] { const char* e = std::getenv("PBVD_HOST_LAST"); return e ? std::atoll(e) : -1; }();
+    int64_t last = env_last >= 0 ? env_last : (nblocks >= 4 * 4096 ? 4096 : 0);
+    if (last >= nblocks) last = 0;
+    const int64_t big_min = 16384;
+    int64_t n_big = env_nseg > 0 ? env_nseg
+                                 : std::max<int64_t>(4, std::min<int64_t>(4 * n_streams,
+                                                                          (nblocks - last) / big_min));
+    n_big = std::max<int64_t>(1, std::min(n_big, nblocks - last));
+    const int64_t seg = (nblocks - last + n_big - 1) / n_big;
+    std::vector<int64_t> seg_b0;
+    for (int64_t b = block0; b < block0 + nblocks - last; b += seg) seg_b0.push_back(b);
+    if (last > 0) seg_b0.push_back(block0 + nblocks - last);
+    const int64_t nseg = int64_t(seg_b0.size());
+    const int64_t seg_max = std::max(seg, last);
     if (!h->h2d && cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) != cudaSuccess) {
         h->prof = prof;
         h->var = var_saved;
@@ -770,20 +789,20 @@ int pbvd_decode_host(pbvd_t h, const int8_t* h_llr_window, int64_t window_stage0
     for (int i = 0; i < n_streams && rc == PBVD_OK; ++i) {
         HostLane& ln = h->lanes[size_t(i)];
         const BlockGeo ga = geo(h, n_info_total, n_stages, nb, block0);
-        const BlockGeo gz = geo(h, n_info_total, n_stages, nb, std::min(block0 + nblocks, block0 + seg) - 1);
+        const BlockGeo gz = geo(h, n_info_total, n_stages, nb, std::min(block0 + nblocks, block0 + seg_max) - 1);
         const int64_t span_max = (gz.hi - ga.lo) + 2 * (h->L + h->V) + h->D;
         rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_llr), &ln.llr_cap,
                         size_t(kept_before_h(h, span_max) + h->R * 16));
         if (!rc) rc = ensure_buf(h, reinterpret_cast<void**>(&ln.d_bits), &ln.bits_cap,
-                                 size_t((seg * h->D + 7) / 8));
+                                 size_t((seg_max * h->D + 7) / 8));
         if (!rc) {
             cudaEventRecord(ln.consumed, ln.stream);   // buffers free
         }
     }
     for (int64_t k = 0; k < nseg && rc == PBVD_OK; ++k) {
         HostLane& ln = h->lanes[size_t(k % n_streams)];
-        const int64_t b0 = block0 + k * seg;
-        const int64_t b1 = std::min(block0 + nblocks, b0 + seg);
+        const int64_t b0 = seg_b0[size_t(k)];
+        const int64_t b1 = (k + 1 < nseg) ? seg_b0[size_t(k + 1)] : block0 + nblocks;
         const BlockGeo ga = geo(h, n_info_total, n_stages, nb, b0);
         const BlockGeo gz = geo(h, n_info_total, n_stages, nb, b1 - 1);
         const int64_t k0 = kept_before_h(h, ga.lo), k1 = kept_before_h(h, gz.hi);
