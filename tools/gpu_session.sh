@@ -1,8 +1,5 @@
 python -m paper_1608_00066_b200.build > /dev/null || exit 1
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_fullsize.py -q -x --timeout 600 -p no:cacheprovider -k host 2>&1 | tail -2
-for r in 1 2; do
-timeout 900 python tools/e2e_sweep.py C2 4,0 0 2>&1
-timeout 900 python tools/e2e_sweep.py C2 0 -1 2>&1
-done | tee gpurun_out/r2z_e2e.txt
-for c in C3a C4; do timeout 900 python tools/e2e_sweep.py $c 0,4 -1,0 2>&1; done | tee -a gpurun_out/r2z_e2e.txt
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv
+PBVD_LIB=$PWD/paper_1608_00066_b200/build/variants/nw4.so timeout 600 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -p no:cacheprovider 2>&1 | tail -1 | sed "s/^/nw4 parity: /"
+CASES="C4 C2 C2:67108864 C3a C4:67108864" bash tools/ab.sh nw4 nw4ns 2>&1 | tee gpurun_out/r2ab_ab.txt
