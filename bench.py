@@ -97,6 +97,13 @@ def describe(c, code, n_total, world):
             f"D={c['D']} L={c['L']}, terminated")
 
 
+def workload_config(c, code, n_total, world):
+    """The bench line's `config`: the workload, the same in both arms."""
+    return {"workload": describe(c, code, n_total, world), "n_info_total": n_total,
+            "D": c["D"], "L": c["L"], "parallelism": f"block-range shards x{world}",
+            "l2": "GPU arm: L2 flushed (256 MiB memset) before every timed step"}
+
+
 class ClockSampler:
     """Samples SM clock and throttle reasons through NVML (every `period` s)
     while running; mark() brackets the timed region, whose samples are also
@@ -350,8 +357,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(secs) * 1e3,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic", "config": {"workload": describe(c, code, n_total, world),
-                                         "impl": "CPU oracle (oracle/pbvd_oracle.c), per-edge ACS"},
+        "data": "synthetic", "config": workload_config(c, code, n_total, world),
+        "run": {"impl": "CPU oracle (oracle/pbvd_oracle.c), per-edge ACS, all host cores"},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -667,10 +674,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "int16",
             "data": "synthetic (seeded BPSK/AWGN, 8-bit quantised)",
-            "config": {"workload": describe(c, code, n_total, world),
-                       "n_info_total": n_total, "D": D, "L": L, "lanes": dec.lanes,
-                       "l2": "flushed (256 MiB memset) before every timed step",
-                       "parallelism": f"block-range shards x{world}",
+            # config: the workload only (identical in both arms); how this arm
+            # ran it is in "run"
+            "config": workload_config(c, code, n_total, world),
+            "run": {"lanes": dec.lanes,
                        "gather": {"none": "none (1 GPU)",
                                   "peer": "fused into the traceback: stores to every rank's "
                                           "buffer over CUDA IPC / NVLink (completion: one "

@@ -66,7 +66,7 @@ def test_bench_two_ranks_gloo(gpu):
     assert "x2" in d["config"]["parallelism"]
     # the default gather: fused into the traceback over CUDA IPC, verified
     # against an NCCL/gloo all_gather after the warm-up (else it falls back)
-    assert d["config"]["gather"].startswith("fused"), d["config"]["gather"]
+    assert d["run"]["gather"].startswith("fused"), d["run"]["gather"]
 
 
 def test_mirrored_outputs_match_oracle(gpu, orc):
@@ -137,6 +137,6 @@ def test_bench_two_gpus_nccl(gather):
     assert d["n_gpus"] == 2 and d["parity"]["bit_exact"]
     assert d["parity"]["blocks_checked"] == d["parity"]["blocks_total"] == 65536
     if gather == "peer":
-        assert d["config"]["gather"].startswith("fused"), d["config"]["gather"]
+        assert d["run"]["gather"].startswith("fused"), d["run"]["gather"]
     else:
-        assert d["config"]["gather"].startswith("NCCL")
+        assert d["run"]["gather"].startswith("NCCL")
