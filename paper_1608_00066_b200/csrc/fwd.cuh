@@ -554,23 +554,34 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     constexpr int GPS = (NG + CF::NCYC - 1) / CF::NCYC;     // groups per pair per slice
     constexpr int TPER = (GPS + W - 1) / W;                 // items per lane per slice
     const int tp = lane % PPW, tsub = lane / PPW;
-    auto transform = [&](int c, int j) {
+    // per-chunk part of the transform (window bases and shifts of this lane's
+    // pair), computed once per chunk rather than once per slice
+    struct TfmSetup {
+        const uint8_t* base[2];
+        uint32_t sh[2];
+        uint32_t* lb;
+    };
+    auto transform_setup = [&](int c) {
+        TfmSetup ts;
         const bool dense = (p.P == 1);            // else read the depunctured dep[]
-        if (edge && tp != 0) return;              // an edge unit has one (replicated) pair
         const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
         const uint8_t* wo = woffs + (c & 1) * BPW;
-        uint32_t* lb = lam + size_t(c & 1) * PPW * LSTR + size_t(tp) * LSTR;
-        constexpr int GW = G * R / 4;                     // words per block per item
-        const uint8_t* base[2];
-        int o0[2];
-        uint32_t sh[2];
+        ts.lb = lam + size_t(c & 1) * PPW * LSTR + size_t(tp) * LSTR;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = edge ? 0 : 2 * tp + h;
-            o0[h] = dense ? int(wo[i]) : 0;
-            base[h] = rb + size_t(CF::wslot(i)) * RAWB + (o0[h] & ~3);
-            sh[h] = uint32_t(o0[h] & 3) * 8u;
+            const int o0 = dense ? int(wo[i]) : 0;
+            ts.base[h] = rb + size_t(CF::wslot(i)) * RAWB + (o0 & ~3);
+            ts.sh[h] = uint32_t(o0 & 3) * 8u;
         }
+        return ts;
+    };
+    auto transform = [&](const TfmSetup& ts, int j) {
+        if (edge && tp != 0) return;              // an edge unit has one (replicated) pair
+        constexpr int GW = G * R / 4;                     // words per block per item
+        const uint8_t* const* base = ts.base;
+        const uint32_t* sh = ts.sh;
+        uint32_t* lb = ts.lb;
 #pragma unroll
         for (int u = 0; u < TPER; ++u) {
             // straight-line: an item past the slice is computed on a clamped
@@ -651,8 +662,11 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             depuncture(0);
             __syncwarp();
         }
+        {
+            const TfmSetup ts0 = transform_setup(0);
 #pragma unroll 1
-        for (int j = 0; j < CF::NCYC; ++j) transform(0, j);
+            for (int j = 0; j < CF::NCYC; ++j) transform(ts0, j);
+        }
         __syncwarp();
         if (!edge && p.pad > 0) {
             // the front pad stages are erasures (lambda = 0, biased u = 128)
@@ -699,6 +713,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             // (within a cycle Cycle<> loads one stage ahead); the read past the
             // chunk's last stage stays inside the operand row's padding
             XY<CF> first = src.load(0);
+            const TfmSetup tsn = transform_setup(c + 1);      // harmless past the last chunk
 #pragma unroll 1
             for (int j = 0; j < ncyc; ++j) {
                 const int s0 = j * V;
@@ -707,7 +722,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                 Cycle<CF, 0, true>::run(pm, src, flip, lg, crow, s0, T, true, first, p.one,
                                         p.neg_one);
                 first = nfirst;
-                transform(c + 1, j);     // harmless past the last chunk
+                transform(tsn, j);
             }
         }
         if (ncyc * V < nst)   // (the last chunk of an edge block)
