@@ -106,6 +106,10 @@ struct Cfg {
     static constexpr int T = V * (cmin(32, (32767 - M0) / (255 * R)) / V);
     static_assert(T >= V, "normalisation period");
     static_assert(M0 + T * 255 * R <= 32767, "int16 headroom");
+    // interior blocks start from all-zero metrics, so after a renormalisation
+    // their metrics are within the state spread <= v*128R (no S_HEAD): when
+    // v*128R + 2T*255R still fits int16 they renormalise every other chunk
+    static constexpr int RN = (V * 128 * R + 2 * T * 255 * R <= 32767) ? 2 : 1;
     // raw window per block and chunk: the T*R soft bytes rounded out to
     // 16-byte vectors (+1 vector for the alignment superset)
     static constexpr int BOXB = ((T * R + 15) / 16) * 16 + 16;
@@ -728,14 +732,17 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         if (ncyc * V < nst)   // (the last chunk of an edge block)
             Cycle<CF, 0, false>::run(pm, src, flip, lg, drow + size_t(ncyc * V) * ROW, ncyc * V, nst, true,
                                      src.load(ncyc * V), p.one, p.neg_one);
-        // renormalise: subtract the block minimum (per 16-bit half = per block)
-        uint32_t mn = pm[0];
+        // renormalise: subtract the block minimum (per 16-bit half = per block);
+        // interior warps every RN chunks (edge warps: head blocks hold S_HEAD)
+        if (edge || CF::RN == 1 || (c % CF::RN) == CF::RN - 1) {
+            uint32_t mn = pm[0];
 #pragma unroll
-        for (int k = 1; k < S; ++k) mn = __vmins2(mn, pm[k]);
+            for (int k = 1; k < S; ++k) mn = __vmins2(mn, pm[k]);
 #pragma unroll
-        for (int o = 1; o < W; o <<= 1) mn = __vmins2(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            for (int o = 1; o < W; o <<= 1) mn = __vmins2(mn, __shfl_xor_sync(0xffffffffu, mn, o));
 #pragma unroll
-        for (int k = 0; k < S; ++k) pm[k] -= mn;
+            for (int k = 0; k < S; ++k) pm[k] -= mn;
+        }
         __syncwarp();      // every lane is done with lam[c & 1] before chunk c+2's transform
     }
 
