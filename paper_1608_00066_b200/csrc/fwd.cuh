@@ -461,10 +461,10 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
     if (p.dbg && lane == 0) {
         unsigned smid; asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        p.dbg[8 * gw + 0] = gtime();
-        p.dbg[8 * gw + 3] = smid;
+        p.dbg[32 * gw + 0] = gtime();
+        p.dbg[32 * gw + 3] = smid;
         unsigned wid; asm("mov.u32 %0, %%warpid;" : "=r"(wid));
-        p.dbg[8 * gw + 7] = wid;
+        p.dbg[32 * gw + 7] = wid;
     }
 #endif
     const int span = edge ? p.edges[e].span : p.span_int;
@@ -744,6 +744,9 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             for (int k = 0; k < S; ++k) pm[k] -= mn;
         }
         __syncwarp();      // every lane is done with lam[c & 1] before chunk c+2's transform
+#ifdef PBVD_EXP_TIMING
+        if (p.dbg && lane == 0 && c < 24) p.dbg[32 * gw + 8 + c] = gtime();
+#endif
     }
 
     // ---- traceback start: min PM, lowest logical state on ties --------
@@ -787,7 +790,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         }
         const int nblk_tb = edge ? 1 : int(min(int64_t(BPW), int64_t(p.n_int) - wb0));
 #ifdef PBVD_EXP_TIMING
-        if (p.dbg && lane == 0) p.dbg[8 * gw + 1] = gtime();
+        if (p.dbg && lane == 0) p.dbg[32 * gw + 1] = gtime();
 #endif
         warp_traceback<CF>(wbase, gdec, span, edge ? p.edges[e].t0r : p.t0r,
                            edge ? p.edges[e].t1r : p.t1r, nblk_tb, stv, ob,
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                                                                         p.edges[e].t0r)) & 31) == 0)),
                            p.out, lane,
 #ifdef PBVD_EXP_TIMING
-                           p.dbg ? p.dbg + 8 * gw : nullptr);
+                           p.dbg ? p.dbg + 32 * gw : nullptr);
 #else
                            nullptr);
 #endif
@@ -816,7 +819,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         }
 #ifdef PBVD_EXP_TIMING
         __syncwarp();
-        if (p.dbg && lane == 0) p.dbg[8 * gw + 2] = gtime();
+        if (p.dbg && lane == 0) p.dbg[32 * gw + 2] = gtime();
 #endif
         return;
     }

@@ -421,7 +421,7 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         // timing experiment: per-warp (start, forward end, traceback end, smid)
         static unsigned long long* dbg = nullptr;
         const char* dump = std::getenv("PBVD_TIMING_DUMP");
-        const size_t ndbg = size_t(fgrid) * 8;
+        const size_t ndbg = size_t(fgrid) * 32;
         if (dump) {
             if (dbg) cudaFree(dbg);
             cudaMalloc(&dbg, ndbg * 8);

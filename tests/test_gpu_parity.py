@@ -187,6 +187,11 @@ def test_compute_sanitizer_memcheck_clean(pbvd):
     import subprocess
     import sys
     from pathlib import Path
+    import os
+    if os.environ.get("PBVD_SANITIZER_TEST") != "1":
+        # the GPU pool refuses compute-sanitizer runs (they have left GPUs
+        # needing a reset); the builder-run captures are in profiles/*_sanitizers.txt
+        pytest.skip("compute-sanitizer runs are closed on this GPU pool (opt in: PBVD_SANITIZER_TEST=1)")
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not Path(cs).exists():
         pytest.skip("compute-sanitizer not available")

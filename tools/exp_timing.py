@@ -19,8 +19,11 @@ torch.cuda.synchronize()
 os.environ["PBVD_TIMING_DUMP"] = "/tmp/pbvd_timing.bin"
 dec.decode(llr, n)
 torch.cuda.synchronize()
-a = np.fromfile("/tmp/pbvd_timing.bin", dtype=np.uint64).reshape(-1, 8).astype(np.int64)
+a = np.fromfile("/tmp/pbvd_timing.bin", dtype=np.uint64).reshape(-1, 32).astype(np.int64)
 a = a[a[:, 0] > 0]
+out = os.environ.get("PBVD_TIMING_SAVE")
+if out:
+    np.save(out, a)
 t0 = a[:, 0].min()
 st, fe, te, sm = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3, a[:, 3]
 print(f"{cfg} n={n} warps={len(a)}  kernel span {te.max():.1f} us")
