@@ -13,7 +13,8 @@ n_info = int(sys.argv[2]) if len(sys.argv) > 2 else c["n_info"]
 info, llr = synth.make_stream(code, n_info, c["ebn0"], c["seed"], punct, c["hard"], device="cuda")
 import os, itertools
 lanes_all = sorted({l for (K, R, p, l) in P.supported() if K == code["K"] and tuple(p) == tuple(code["polys"])})
-for fused, lanes in itertools.product([int(x) for x in os.environ.get("QT_FUSED", "1").split()], lanes_all):
+lanes_sel = [int(x) for x in os.environ.get("QT_LANES", "").split()] or lanes_all
+for fused, lanes in itertools.product([int(x) for x in os.environ.get("QT_FUSED", "1").split()], lanes_sel):
     dec = P.Decoder(code["K"], code["polys"], c["D"], c["L"], punct=punct, lanes=lanes, fused=bool(fused))
     dec.set_profiling(True)
     out = dec.decode(llr, n_info)
