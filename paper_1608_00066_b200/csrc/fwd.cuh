@@ -651,8 +651,23 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         pm[k] = head ? ((lg == 0 && k == 0) ? 0u : uint32_t(S_HEAD) * 0x00010001u) : 0u;
 
     uint32_t* gdec = nullptr;
+    // survivor region of an interior job; with recycling (fused streams
+    // larger than the workspace) wait until the region's previous job has
+    // finished its traceback -- it was launched n_regions jobs earlier, so
+    // it is running or done and never waits on this one
+    size_t region = size_t(gw);
+    unsigned region_use = 0;
+    if (FUSED && !edge && p.n_regions > 0) {
+        region = size_t(gw % p.n_regions);
+        region_use = unsigned(gw / p.n_regions);
+        if (region_use > 0) {
+            // every lane polls (one transaction): a warp-uniform loop
+            while (!__all_sync(0xffffffffu, ld_acquire_u32(p.region_done + region) >= region_use))
+                __nanosleep(256);
+        }
+    }
     if (!edge) {
-        gdec = p.dec + size_t(gw) * size_t(p.span_int) * ROW;
+        gdec = p.dec + region * size_t(p.span_int) * ROW;
     } else {
         gdec = p.dec_edge + size_t(e) * size_t(p.span_edge_max) * ROW;
     }
@@ -802,6 +817,12 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
 #else
                            nullptr);
 #endif
+        if (!edge && p.n_regions > 0) {
+            // the region's rows have all been read (every bulk copy of the
+            // walk was waited for): the next job in it may overwrite them
+            __syncwarp();
+            if (lane == 0) st_release_u32(p.region_done + region, region_use + 1u);
+        }
         if constexpr (MIRROR) {
             // multi-GPU gather fused into this kernel: the warp's decoded
             // bytes (its blocks own whole, contiguous bytes) go to every

@@ -79,6 +79,12 @@ struct FwdParams {
     int start_zero;        // 1: every traceback starts in state 0 (PBVD_START_ZERO)
     int n_mirror;          // extra output destinations (fused mode, mirror_copy)
     int64_t mirror[MAX_MIRROR];   // byte offsets of the destinations from out
+    // fused mode, streams larger than the survivor workspace: interior job
+    // gw uses region gw % n_regions once the job before it there (gw -
+    // n_regions) has finished its traceback (region_done[r] counts the jobs
+    // done in region r this launch); 0: region = gw (one region per job)
+    int n_regions;
+    unsigned* region_done;
     unsigned long long* dbg;   // timing experiment only (PBVD_EXP_TIMING builds), else null
     EdgeDesc edges[MAX_EDGE];
 };

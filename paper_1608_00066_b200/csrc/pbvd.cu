@@ -347,8 +347,16 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         std::vector<int64_t> eblk;      // block index of each edge
     };
     std::vector<Group> groups;
-    for (int64_t d0 = 0; d0 < n_int || (n_int == 0 && groups.empty()); d0 += wave) {
-        groups.push_back({I0 + d0, I0 + std::min(n_int, d0 + wave), {}, {}});
+    // fused mode: a stream larger than one wave runs as ONE launch whose jobs
+    // recycle the wave's survivor regions (job gw -> region gw % regions,
+    // after the region's previous job has traced back), so there is a single
+    // grid tail instead of one per wave; two-kernel mode keeps waves (its
+    // traceback grid needs every region of the wave at once)
+    static const bool env_recycle = [] { const char* e = std::getenv("PBVD_RECYCLE"); return !e || std::atoi(e) != 0; }();
+    const bool recycle = h->fused && env_recycle && n_int > wave;
+    const int64_t launch_blocks = recycle ? n_int : wave;
+    for (int64_t d0 = 0; d0 < n_int || (n_int == 0 && groups.empty()); d0 += launch_blocks) {
+        groups.push_back({I0 + d0, I0 + std::min(n_int, d0 + launch_blocks), {}, {}});
         if (n_int == 0) break;
     }
     const int64_t n_head = I0 - B0;
@@ -415,6 +423,15 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
             tp.edges[i] = g.edges[size_t(i)];
         }
         const int fgrid = int((fp.n_int_warps + ne + v->NT / 32 - 1) / (v->NT / 32));
+        fp.n_regions = 0;
+        fp.region_done = nullptr;
+        if (recycle && fp.n_int_warps > wave_regions) {
+            // the two-kernel start array is free in fused mode: region counters
+            fp.n_regions = int(wave_regions);
+            fp.region_done = reinterpret_cast<unsigned*>(start_int);
+            cudaError_t me = cudaMemsetAsync(fp.region_done, 0, size_t(wave_regions) * 4, stream);
+            if (me != cudaSuccess) return cuda_fail(h, me, "cudaMemsetAsync (region counters)");
+        }
         const int ev = record(h, stream);
         if (ev >= 0) cudaEventRecord(h->ev_pool[ev], stream);
 #ifdef PBVD_EXP_TIMING

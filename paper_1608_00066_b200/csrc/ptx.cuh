@@ -118,4 +118,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
         "}\n" ::"r"(mbar), "r"(parity) : "memory");
 }
 
+// ---- survivor-region recycling (gpu-scope acquire / release) ---------------
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 }  // namespace pbvd
