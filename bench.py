@@ -427,6 +427,7 @@ def run_ours(args):
     elif gather_mode == "nccl":
         gather_note = "forced by PBVD_BENCH_GATHER=nccl"
     done_flag = torch.zeros(1, dtype=torch.int32, device=cdev)
+    align_flag = torch.zeros(1, dtype=torch.int32, device=cdev)
 
     def decode_part():
         if gather_mode == "peer":
@@ -489,6 +490,11 @@ def run_ours(args):
         # L2 flush; the host enqueues the decode while the memset runs, so
         # the timed region holds no host launch latency
         flush.zero_()
+        if world > 1:
+            # device-side start line: one-word all_reduce queued after the
+            # flush, so every rank's timed region starts when all GPUs are
+            # ready (host wake-up skew after the barrier is not decode time)
+            dist.all_reduce(align_flag)
         e0 = torch.cuda.Event(enable_timing=True)
         em = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -684,7 +690,7 @@ def run_ours(args):
                                           "all_reduce word behind the decode)",
                                   "nccl": "NCCL all_gather"}[gather_mode] +
                                  (f" [{gather_note}]" if gather_note else ""),
-                       "step_barrier": "dist.barrier + synchronize before every timed step"
+                       "step_barrier": "dist.barrier + synchronize before every timed step, then a one-word device all_reduce after the L2 flush as the start line of the timed region"
                                        if world > 1 else "none (1 GPU)"},
             "t_G": {"decode_ms": dec_ms_tot / args.steps, "gather_ms": gat_ms_tot / args.steps,
                     "note": "per step, each the max over ranks of its CUDA-event time on the "
