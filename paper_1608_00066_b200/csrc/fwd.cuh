@@ -661,9 +661,15 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         region = size_t(gw % p.n_regions);
         region_use = unsigned(gw / p.n_regions);
         if (region_use > 0) {
-            // every lane polls (one transaction): a warp-uniform loop
-            while (!__all_sync(0xffffffffu, ld_acquire_u32(p.region_done + region) >= region_use))
+            // every lane polls (one transaction): a warp-uniform loop; a
+            // region that never frees (impossible unless the grid's blocks
+            // were dispatched out of order) traps after ~1 s instead of
+            // hanging the device
+            for (unsigned spin = 0;
+                 !__all_sync(0xffffffffu, ld_acquire_u32(p.region_done + region) >= region_use); ++spin) {
+                if (spin > (1u << 22)) __trap();
                 __nanosleep(256);
+            }
         }
     }
     if (!edge) {
