@@ -219,14 +219,17 @@ void mkdirs(const std::string& d) {
         if (k == d.size() || d[k] == '/') mkdir(d.substr(0, k).c_str(), 0755);
 }
 
-// cache file: "PBVDJIT2\n" + 4 lowered names (one per line) + cubin bytes
-constexpr char MAGIC[] = "PBVDJIT2\n";
+// kernels per variant: fwd, fused, fused+mirror, traceback, fused+recycle
+constexpr int NKERN = 5;
 
-bool cache_load(const std::string& path, std::string names[4], std::string* cubin) {
+// cache file: "PBVDJIT3\n" + NKERN lowered names (one per line) + cubin bytes
+constexpr char MAGIC[] = "PBVDJIT3\n";
+
+bool cache_load(const std::string& path, std::string names[NKERN], std::string* cubin) {
     std::string all;
     if (!read_file(path, &all) || all.compare(0, sizeof MAGIC - 1, MAGIC) != 0) return false;
     size_t pos = sizeof MAGIC - 1;
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NKERN; ++i) {
         const size_t e = all.find('\n', pos);
         if (e == std::string::npos) return false;
         names[i] = all.substr(pos, e - pos);
@@ -236,14 +239,15 @@ bool cache_load(const std::string& path, std::string names[4], std::string* cubi
     return !cubin->empty();
 }
 
-void cache_store(const std::string& dir, const std::string& path, const std::string names[4],
+void cache_store(const std::string& dir, const std::string& path, const std::string names[NKERN],
                  const std::string& cubin) {
     mkdirs(dir);
     const std::string tmp = path + ".tmp" + std::to_string(getpid());
     {
         std::ofstream f(tmp, std::ios::binary);
         if (!f) return;
-        f << MAGIC << names[0] << '\n' << names[1] << '\n' << names[2] << '\n' << names[3] << '\n';
+        f << MAGIC;
+        for (int i = 0; i < NKERN; ++i) f << names[i] << '\n';
         f.write(cubin.data(), std::streamsize(cubin.size()));
         if (!f) return;
     }
@@ -263,7 +267,7 @@ std::vector<std::unique_ptr<JitEntry>> g_jit;
 
 // NVRTC build (or disk-cache hit) of the three kernels of (K, R, polys, W):
 // cubin + lowered names.  Needs no GPU.
-bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[4],
+bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[NKERN],
                  std::string* cubin, std::string* err) {
     auto fail = [&](const std::string& m) {
         if (err) *err = m;
@@ -273,10 +277,11 @@ bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[4
     char cfg[160];
     std::snprintf(cfg, sizeof cfg, "pbvd::Cfg<pbvd::Code<%d, %d, %uu, %uu, %uu, %uu>, %d>", K, R,
                   polys[0], polys[1], R > 2 ? polys[2] : 0u, R > 3 ? polys[3] : 0u, W);
-    const std::string exprs[4] = {std::string("pbvd::fwd_kernel<") + cfg + ", false>",
-                                  std::string("pbvd::fwd_kernel<") + cfg + ", true>",
-                                  std::string("pbvd::fwd_kernel<") + cfg + ", true, true>",
-                                  std::string("pbvd::tb_kernel<") + cfg + ">"};
+    const std::string exprs[NKERN] = {std::string("pbvd::fwd_kernel<") + cfg + ", false>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true>",
+                                      std::string("pbvd::tb_kernel<") + cfg + ">",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, false, true>"};
     const std::string source = "// pbvd JIT: " + std::string(cfg) +
                                "\n#include \"fwd.cuh\"\n#include \"tb.cuh\"\n";
     const std::string sdir = src_dir();
@@ -322,7 +327,7 @@ bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[4
         if (log.size() > 4000) log = log.substr(0, 4000) + "...";
         return fail(std::string("JIT: NVRTC compile failed: ") + n.errstr(r) + "\n" + log);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NKERN; ++i) {
         const char* low = nullptr;
         if (n.lowered(prog, exprs[i].c_str(), &low) != NVRTC_SUCCESS || !low) {
             n.destroy(&prog);
@@ -355,7 +360,7 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
         if (same) return &e->v;
     }
     auto ent = std::make_unique<JitEntry>();
-    std::string names[4];
+    std::string names[NKERN];
     if (!jit_compile(K, R, polys, W, names, &ent->cubin, err)) return nullptr;
     cudaError_t e = cudaLibraryLoadData(&ent->lib, ent->cubin.data(), nullptr, nullptr, 0, nullptr,
                                         nullptr, 0);
@@ -363,8 +368,8 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
         cudaGetLastError();
         return fail(std::string("JIT: cudaLibraryLoadData: ") + cudaGetErrorString(e));
     }
-    cudaKernel_t ks[4] = {};
-    for (int i = 0; i < 4; ++i) {
+    cudaKernel_t ks[NKERN] = {};
+    for (int i = 0; i < NKERN; ++i) {
         e = cudaLibraryGetKernel(&ks[i], ent->lib, names[i].c_str());
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -379,6 +384,7 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
     ent->v.k_fused = reinterpret_cast<const void*>(ks[1]);
     ent->v.k_mirror = reinterpret_cast<const void*>(ks[2]);
     ent->v.k_tb = reinterpret_cast<const void*>(ks[3]);
+    ent->v.k_recycle = reinterpret_cast<const void*>(ks[4]);
     ent->v.prepared = 0;
     g_jit.push_back(std::move(ent));
     return &g_jit.back()->v;
@@ -395,7 +401,7 @@ extern "C" int pbvd_jit_prebuild(int K, int R, const uint32_t* polys, int lanes,
     const int W = lanes == 0 ? pbvd::default_lanes(K) : lanes;
     pbvd::Variant shape{};
     std::string err;
-    std::string names[4], cubin;
+    std::string names[pbvd::NKERN], cubin;
     int rc = PBVD_OK;
     if (!pbvd::variant_shape(K, R, W, &shape)) {
         err = "no kernel shape for that (K, R, lanes)";

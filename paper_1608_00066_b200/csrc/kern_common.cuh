@@ -36,7 +36,7 @@ void fill_shape(Variant& v) {
     v.smem_fused = fused_smem<CF>();
     v.default_rank = 0;
     v.jit = false;
-    v.k_fwd = v.k_fused = v.k_mirror = v.k_tb = nullptr;
+    v.k_fwd = v.k_fused = v.k_mirror = v.k_recycle = v.k_tb = nullptr;
     v.prepared = 0;
 }
 
@@ -49,6 +49,7 @@ Variant make_variant(int rank) {
     v.k_fwd = reinterpret_cast<const void*>(&fwd_kernel<CF, false>);
     v.k_fused = reinterpret_cast<const void*>(&fwd_kernel<CF, true>);
     v.k_mirror = reinterpret_cast<const void*>(&fwd_kernel<CF, true, true>);
+    v.k_recycle = reinterpret_cast<const void*>(&fwd_kernel<CF, true, false, true>);
     v.k_tb = reinterpret_cast<const void*>(&tb_kernel<CF>);
     return v;
 }

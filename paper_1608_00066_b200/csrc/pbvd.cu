@@ -139,9 +139,10 @@ int ensure_prepared(pbvd_t h, const Variant* v) {
     std::lock_guard<std::mutex> lk(g_prep_mu);
     const uint64_t bit = uint64_t(1) << (h->device & 63);
     if (!(v->prepared & bit)) {
-        const std::pair<const void*, size_t> ks[4] = {{v->k_fwd, fwd_smem(v->smem_fwd)},
+        const std::pair<const void*, size_t> ks[5] = {{v->k_fwd, fwd_smem(v->smem_fwd)},
                                                        {v->k_fused, fwd_smem(v->smem_fused)},
                                                        {v->k_mirror, fwd_smem(v->smem_fused)},
+                                                       {v->k_recycle, fwd_smem(v->smem_fused)},
                                                        {v->k_tb, v->smem_tb}};
         for (const auto& k : ks) {
             cudaError_t e = cudaFuncSetAttribute(k.first, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -446,7 +447,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
             fp.dbg = dbg;
         }
 #endif
-        cudaError_t le = h->fused ? launch(fp.n_mirror > 0 ? v->k_mirror : v->k_fused, fgrid, v->NT,
+        cudaError_t le = h->fused ? launch(fp.n_mirror > 0 ? v->k_mirror
+                                           : fp.n_regions > 0 ? v->k_recycle : v->k_fused, fgrid, v->NT,
                                            fwd_smem(v->smem_fused), stream, fp, false)
                                   : launch(v->k_fwd, fgrid, v->NT, fwd_smem(v->smem_fwd), stream, fp,
                                            false);

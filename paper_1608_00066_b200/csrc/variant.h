@@ -29,7 +29,8 @@ struct Variant {
     // cudaFuncSetAttribute / cudaLaunchKernelExC
     const void* k_fwd;      // fwd_kernel<CF, false>(FwdParams)
     const void* k_fused;    // fwd_kernel<CF, true>(FwdParams)
-    const void* k_mirror;   // fwd_kernel<CF, true, true>(FwdParams): fused + mirror copies
+    const void* k_mirror;   // fwd_kernel<CF, true, true>(FwdParams): fused + mirror copies (+ region recycling)
+    const void* k_recycle;  // fwd_kernel<CF, true, false, true>(FwdParams): fused, recycled survivor regions
     const void* k_tb;       // tb_kernel<CF>(TbParams)
     mutable uint64_t prepared;   // per-device bit: dynamic smem attribute set
 };
