@@ -96,6 +96,30 @@ def test_mirrored_outputs_match_oracle(gpu, orc):
             dec.decode_blocks_mirrored(llr, 0, n_info, 0, nb, out, [m1.data_ptr() + 1])
 
 
+def test_mirrored_outputs_with_recycled_regions(gpu, orc):
+    """The mirrored kernel on a range larger than its survivor workspace
+    (1 MiB: 6 regions for 128 jobs, so its jobs recycle regions within the one
+    launch): every destination equal to the oracle's bits."""
+    sys.path.insert(0, str(ROOT))
+    import synth
+    import paper_1608_00066_b200 as P
+    code = synth.CODES["k7"]
+    n_info, D, L = 1 << 21, 512, 42
+    info, llr = synth.make_stream(code, n_info, 3.0, 67, device="cuda")
+    want = torch.from_numpy(orc.pack_bits(orc.decode(code, llr.cpu().numpy(), n_info, D, L))).cuda()
+    dec = P.Decoder(7, code["polys"], D, L)
+    dec.set_workspace_limit(1 << 20)
+    dec.set_profiling(True)
+    nb = dec.block_count(n_info)
+    out = torch.zeros(want.numel(), dtype=torch.uint8, device="cuda")
+    m1 = torch.zeros(want.numel() + 4, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        dec.decode_blocks_mirrored(llr, 0, n_info, 0, nb, out, [m1.data_ptr() + 4])
+    torch.cuda.synchronize()
+    assert dec.kernel_times()[2] == 1          # one launch, regions recycled
+    assert torch.equal(out, want) and torch.equal(m1[4:], want)
+
+
 def test_ipc_export_open_roundtrip(gpu):
     """pbvd_ipc_export of a pointer inside a torch allocation gives the
     allocation's handle and the pointer's offset (the bench's peer gather
