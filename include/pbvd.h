@@ -234,7 +234,9 @@ int pbvd_get_fused(pbvd_t h);
 
 /* Upper bound on the survivor workspace in bytes (default 4 GiB: measured
  * best for C5 on B200 -- larger waves lose to address-translation misses);
- * decodes larger than one workspace run in waves.  Returns PBVD_EINVAL below
+ * decodes larger than one workspace run, in fused mode, as one launch whose
+ * jobs recycle the workspace's survivor regions, and in two-kernel mode in
+ * waves.  Returns PBVD_EINVAL below
  * 1 MiB. */
 int pbvd_set_workspace_limit(pbvd_t h, size_t bytes);
 
