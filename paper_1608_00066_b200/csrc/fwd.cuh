@@ -138,7 +138,8 @@ struct Cfg {
     static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
     static constexpr size_t WLAM = size_t(2) * PPW * LSTR * 4;   // double buffered
     static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
-    static constexpr size_t WSMEM = ((WRAW + WLAM + WDEP + WOFF + 127) / 128) * 128;
+    static constexpr size_t WPQ = ((WRAW + WLAM + WDEP + WOFF + 7) / 8) * 8;   // offset of [BPW] int64 + [BPW] int
+    static constexpr size_t WSMEM = ((WPQ + size_t(12) * BPW + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
 
     // alpha of the butterfly whose E slot has register index k, restricted
@@ -453,6 +454,8 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [2][PPW][LSTR]
     uint8_t* dep = wbase + CF::WRAW + CF::WLAM;                             // [BPW][RAWB]
     uint8_t* woffs = dep + CF::WDEP;                                        // [2][BPW]
+    int64_t* pq_s = reinterpret_cast<int64_t*>(wbase + CF::WPQ);            // [BPW] (punctured codes)
+    int* pr_s = reinterpret_cast<int*>(wbase + CF::WPQ + 8 * BPW);          // [BPW]
 
     // warp unit: interior warps first (BPW consecutive interior blocks), then
     // one unit per edge block (all lane groups replicate that block)
@@ -485,6 +488,34 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     const int nblk = edge ? 1 : BPW;
     const uintptr_t vlo = reinterpret_cast<uintptr_t>(p.llr);
     const uintptr_t vhi = vlo + uintptr_t(p.n_llr);
+    // lane blocks i = lane + 32 m; punctured codes: each block's position in
+    // the puncture period, split once per job (the only 64-bit division) and
+    // kept in shared memory, so a chunk's kept index needs 32-bit arithmetic
+    // only (the per-chunk 64-bit divisions cost C3 2 %)
+    constexpr int NBL_L = (BPW + 31) / 32;
+    if (p.P != 1) {
+#pragma unroll
+        for (int m = 0; m < NBL_L; ++m) {
+            const int i = lane + 32 * m;
+            if (i < nblk) {
+                const int64_t lo = block_lo(i);
+                int64_t q = lo / p.P;
+                int r = int(lo - q * p.P);
+                if (r < 0) { r += p.P; --q; }   // floor (the first block's front pad may start before 0)
+                pq_s[i] = q;
+                pr_s[i] = r;
+            }
+        }
+    }
+    // kept index (relative to the launch window) of stage s0 >= 0 of lane block i
+    // (only lane i's own entries are read: no barrier needed)
+    auto kept_at = [&](int i, int s0) -> int64_t {
+        if (p.P == 1) return (block_lo(i) + s0) * R - p.kb_ws0;
+        const unsigned u = unsigned(pr_s[i] + s0);
+        const unsigned q = u / unsigned(p.P);
+        const unsigned r = u - q * unsigned(p.P);
+        return (pq_s[i] + int64_t(q)) * p.kp + p.cum[r] - p.kb_ws0;
+    };
 
     // 16-byte cp.async of chunk c's soft windows: lane i copies block i's
     // window (rounded out to 16-byte vectors) to raw[c & 1][i]
@@ -492,9 +523,11 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         const int s0 = c * T;
         const int nst = min(T, span - s0);
         uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
-        for (int i = lane; i < nblk; i += 32) {
-            const int64_t a = block_lo(i) + s0;
-            const int64_t k0 = kept_before(p, a, R) - p.kb_ws0;
+#pragma unroll
+        for (int m = 0; m < NBL_L; ++m) {
+            const int i = lane + 32 * m;
+            if (i >= nblk) break;
+            const int64_t k0 = kept_at(i, s0);
             const uintptr_t ga = (vlo + uintptr_t(k0)) & ~uintptr_t(15);
             uint8_t* dst = rb + size_t(CF::wslot(i)) * RAWB;
             woffs[(c & 1) * BPW + i] = uint8_t((vlo + uintptr_t(k0)) & 15);
@@ -504,7 +537,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                 for (int j = 0; j < RAWB / 16; ++j)
                     cp_async16(smem_u32(dst + 16 * j), reinterpret_cast<const void*>(ga + 16 * j));
             } else {
-                const int64_t k1 = kept_before(p, a + max(nst, 0), R) - p.kb_ws0;
+                const int64_t k1 = kept_at(i, s0 + max(nst, 0));
                 const uintptr_t gb = (vlo + uintptr_t(k1) + 15) & ~uintptr_t(15);
                 for (uintptr_t x = ga; x < gb; x += 16, dst += 16) {
                     if (x >= vlo && x + 16 <= vhi) {
@@ -520,11 +553,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         }
         cp_async_commit();
     };
-    // soft window offset (bytes) of block i in raw[.] for chunk c
-    auto win_off = [&](int i, int64_t a) -> int {
-        const int64_t kw = kept_before(p, a, R) - p.kb_ws0;
-        return int((vlo + uintptr_t(kw)) & 15);
-    };
     // punctured codes: expand chunk c's kept values of every block to a dense
     // [stage][r] byte window in dep[block] (erasure = 0), lane = block (c-18)
     auto depuncture = [&](int c) {
@@ -535,12 +563,15 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         // PRMT-ed with the (phase, word) selector of the host table -- all
         // words independent (no serial kept-index chain)
         constexpr int NWD = (T * R + 3) / 4;
-        for (int i = lane; i < nblk; i += 32) {
-            const int64_t a = block_lo(i) + s0;
-            const int woff = win_off(i, a);
+#pragma unroll
+        for (int m = 0; m < NBL_L; ++m) {
+            const int i = lane + 32 * m;
+            if (i >= nblk) break;
+            // window offset stored by issue_raw(c); phase of the chunk's first stage
+            const int woff = woffs[(c & 1) * BPW + i];
             const uint32_t* win = reinterpret_cast<const uint32_t*>(rb + size_t(CF::wslot(i)) * RAWB);
             uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(CF::wslot(i)) * RAWB);
-            const uint32_t* tab = p.dtab + int(((a % p.P) + p.P) % p.P) * NWD;
+            const uint32_t* tab = p.dtab + int(unsigned(pr_s[i] + s0) % unsigned(p.P)) * NWD;
             const int nw = (nst * R + 3) / 4;
 #pragma unroll 4
             for (int w = 0; w < nw; ++w) {
