@@ -125,7 +125,7 @@ struct Cfg {
     // across pairs) and, for LW = 2 (8-byte per-stage reads) or PPW <= 16,
     // stay 8-byte aligned
     static constexpr int LSTR = ((NG * G * LW + 31) / 32) * 32 + cmax(32 / PPW, LW);
-    // per warp: raw windows [2][BPW][RAWB], operands [2][PPW][LSTR], depunctured [BPW][RAWB]
+    // per warp: raw windows [2][BPW][RAWB], operands [2][PPW][LSTR]
     static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
     // window slot of block i in raw[.] / dep[]: even blocks first, then odd
     // (h-major), so the PPW pairs' same-half windows are RAWB apart and a
@@ -135,10 +135,9 @@ struct Cfg {
         return (i & 1) * PPW + (i >> 1);
     }
     static constexpr size_t WRAW = size_t(2) * BPW * RAWB;         // double buffered
-    static constexpr size_t WDEP = size_t(BPW) * RAWB;             // depunctured window
     static constexpr size_t WLAM = size_t(2) * PPW * LSTR * 4;   // double buffered
     static constexpr size_t WOFF = size_t(2) * BPW;                 // window byte offsets
-    static constexpr size_t WPQ = ((WRAW + WLAM + WDEP + WOFF + 7) / 8) * 8;   // offset of [BPW] int64 + [BPW] int
+    static constexpr size_t WPQ = ((WRAW + WLAM + WOFF + 7) / 8) * 8;   // offset of [BPW] int64 + [BPW] int
     static constexpr size_t WSMEM = ((WPQ + size_t(12) * BPW + 127) / 128) * 128;
     static constexpr size_t SMEM = NWARP * WSMEM;
 
@@ -452,8 +451,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     uint8_t* wbase = smem + size_t(warp) * CF::WSMEM;
     uint8_t* raw = wbase;                                                   // [2][BPW][RAWB]
     uint32_t* lam = reinterpret_cast<uint32_t*>(wbase + CF::WRAW);          // [2][PPW][LSTR]
-    uint8_t* dep = wbase + CF::WRAW + CF::WLAM;                             // [BPW][RAWB]
-    uint8_t* woffs = dep + CF::WDEP;                                        // [2][BPW]
+    uint8_t* woffs = wbase + CF::WRAW + CF::WLAM;                           // [2][BPW]
     int64_t* pq_s = reinterpret_cast<int64_t*>(wbase + CF::WPQ);            // [BPW] (punctured codes)
     int* pr_s = reinterpret_cast<int*>(wbase + CF::WPQ + 8 * BPW);          // [BPW]
 
@@ -553,35 +551,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         }
         cp_async_commit();
     };
-    // punctured codes: expand chunk c's kept values of every block to a dense
-    // [stage][r] byte window in dep[block] (erasure = 0), lane = block (c-18)
-    auto depuncture = [&](int c) {
-        const int s0 = c * T;
-        const int nst = min(T, span - s0);
-        const uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
-        // table-driven: every dense word is one funnel-shifted window word
-        // PRMT-ed with the (phase, word) selector of the host table -- all
-        // words independent (no serial kept-index chain)
-        constexpr int NWD = (T * R + 3) / 4;
-#pragma unroll
-        for (int m = 0; m < NBL_L; ++m) {
-            const int i = lane + 32 * m;
-            if (i >= nblk) break;
-            // window offset stored by issue_raw(c); phase of the chunk's first stage
-            const int woff = woffs[(c & 1) * BPW + i];
-            const uint32_t* win = reinterpret_cast<const uint32_t*>(rb + size_t(CF::wslot(i)) * RAWB);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(dep + size_t(CF::wslot(i)) * RAWB);
-            const uint32_t* tab = p.dtab + int(unsigned(pr_s[i] + s0) % unsigned(p.P)) * NWD;
-            const int nw = (nst * R + 3) / 4;
-#pragma unroll 4
-            for (int w = 0; w < nw; ++w) {
-                const uint32_t e = __ldg(tab + w);
-                const int q = woff + int(e >> 16);
-                const uint32_t x = __funnelshift_r(win[q >> 2], win[(q >> 2) + 1], uint32_t(q & 3) * 8u);
-                dst[w] = prmt(x, 0u, e & 0xffffu);
-            }
-        }
-    };
     // Transform of chunk c, slice j of NCYC: the soft bytes of every (pair,
     // stage) are interleaved A/B, biased by +128 (u = lam ^ 0x80) and stored
     // as LW words to lam[c & 1][pair][stage].  One item = (pair, G stages) =
@@ -599,22 +568,38 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         uint32_t sh[2];
         uint32_t* lb;
     };
+    // punctured codes (c-18): every dense word is depunctured on the fly from
+    // the raw window -- a host table entry per (chunk start phase, dense word)
+    // holds a PRMT selector over four consecutive kept bytes and the first
+    // kept index (erasures select a byte of a zero operand) -- inside the
+    // transform slices, so it overlaps the ACS cycles; sh[h] then packs the
+    // table row (phase * NWD) << 8 and the window's byte offset
+    constexpr int NWD = (T * R + 3) / 4;
     auto transform_setup = [&](int c) {
         TfmSetup ts;
-        const bool dense = (p.P == 1);            // else read the depunctured dep[]
-        const uint8_t* rb = dense ? raw + size_t(c & 1) * BPW * RAWB : dep;
+        const uint8_t* rb = raw + size_t(c & 1) * BPW * RAWB;
         const uint8_t* wo = woffs + (c & 1) * BPW;
         ts.lb = lam + size_t(c & 1) * PPW * LSTR + size_t(tp) * LSTR;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = edge ? 0 : 2 * tp + h;
-            const int o0 = dense ? int(wo[i]) : 0;
-            ts.base[h] = rb + size_t(CF::wslot(i)) * RAWB + (o0 & ~3);
-            ts.sh[h] = uint32_t(o0 & 3) * 8u;
+            const int o0 = int(wo[i]);
+            if (p.P == 1) {
+                ts.base[h] = rb + size_t(CF::wslot(i)) * RAWB + (o0 & ~3);
+                ts.sh[h] = uint32_t(o0 & 3) * 8u;
+            } else {
+                const unsigned ph = unsigned(pr_s[i] + c * T) % unsigned(p.P);
+                ts.base[h] = rb + size_t(CF::wslot(i)) * RAWB;
+                ts.sh[h] = ((ph * unsigned(NWD)) << 8) | unsigned(o0);
+            }
         }
         return ts;
     };
-    auto transform = [&](const TfmSetup& ts, int j) {
+    // PUNCT (compile time): the cycle loop exists twice, dense and punctured,
+    // selected once per chunk -- a run-time test inside the loop body split it
+    // into basic blocks and cost the dense hot loop 62 instructions
+    auto transform = [&](const TfmSetup& ts, int j, auto punct_tag) {
+        constexpr bool PUNCT = decltype(punct_tag)::value;
         if (edge && tp != 0) return;              // an edge unit has one (replicated) pair
         constexpr int GW = G * R / 4;                     // words per block per item
         const uint8_t* const* base = ts.base;
@@ -629,15 +614,31 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             const bool valid = gl < GPS && g0 < NG;
             const int g = valid ? g0 : j * GPS;
             uint32_t v[2][GW];
+            if constexpr (!PUNCT) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(base[h] + 4 * GW * g);
-                uint32_t wl = w[0];
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(base[h] + 4 * GW * g);
+                    uint32_t wl = w[0];
 #pragma unroll
-                for (int k = 0; k < GW; ++k) {
-                    const uint32_t wh = w[k + 1];
-                    v[h][k] = __funnelshift_r(wl, wh, sh[h]) ^ 0x80808080u;   // u = lam + 128
-                    wl = wh;
+                    for (int k = 0; k < GW; ++k) {
+                        const uint32_t wh = w[k + 1];
+                        v[h][k] = __funnelshift_r(wl, wh, sh[h]) ^ 0x80808080u;   // u = lam + 128
+                        wl = wh;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t* win = reinterpret_cast<const uint32_t*>(base[h]);
+                    const uint32_t* tab = p.dtab + (sh[h] >> 8);
+                    const int woff = int(sh[h] & 0xffu);
+#pragma unroll
+                    for (int k = 0; k < GW; ++k) {
+                        const uint32_t e = __ldg(tab + GW * g + k);
+                        const int q = woff + int(e >> 16);
+                        const uint32_t x = __funnelshift_r(win[q >> 2], win[(q >> 2) + 1], uint32_t(q & 3) * 8u);
+                        v[h][k] = prmt(x, 0u, e & 0xffffu) ^ 0x80808080u;
+                    }
                 }
             }
             uint32_t ow[G * LW];
@@ -717,14 +718,13 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         if (nchunks > 1) issue_raw(1);
         if (nchunks > 1) cp_async_wait<1>(); else cp_async_wait<0>();
         __syncwarp();
-        if (p.P != 1) {
-            depuncture(0);
-            __syncwarp();
-        }
         {
             const TfmSetup ts0 = transform_setup(0);
 #pragma unroll 1
-            for (int j = 0; j < CF::NCYC; ++j) transform(ts0, j);
+            for (int j = 0; j < CF::NCYC; ++j) {
+                if (p.P == 1) transform(ts0, j, std::false_type{});
+                else transform(ts0, j, std::true_type{});
+            }
         }
         __syncwarp();
         if (!edge && p.pad > 0) {
@@ -748,10 +748,6 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                 cp_async_wait<0>();
             }
             __syncwarp();
-            if (next && p.P != 1) {
-                depuncture(c + 1);
-                __syncwarp();
-            }
             src.lamrow = lam + size_t(c & 1) * PPW * LSTR + size_t(edge ? 0 : grp) * LSTR;
         }
         // survivor rows of this chunk, this lane's WPS words (direct stores:
@@ -771,18 +767,22 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             // each cycle's first-stage operands are loaded one cycle ahead
             // (within a cycle Cycle<> loads one stage ahead); the read past the
             // chunk's last stage stays inside the operand row's padding
-            XY<CF> first = src.load(0);
             const TfmSetup tsn = transform_setup(c + 1);      // harmless past the last chunk
+            auto cycles = [&](auto punct_tag) {
+                XY<CF> first = src.load(0);
 #pragma unroll 1
-            for (int j = 0; j < ncyc; ++j) {
-                const int s0 = j * V;
-                const XY<CF> nfirst = src.load(s0 + V);
-                uint32_t* crow = (s0 + V > st_lo) ? drow + size_t(s0) * ROW : drow0;
-                Cycle<CF, 0, true>::run(pm, src, flip, lg, crow, s0, T, true, first, p.one,
-                                        p.neg_one);
-                first = nfirst;
-                transform(tsn, j);
-            }
+                for (int j = 0; j < ncyc; ++j) {
+                    const int s0 = j * V;
+                    const XY<CF> nfirst = src.load(s0 + V);
+                    uint32_t* crow = (s0 + V > st_lo) ? drow + size_t(s0) * ROW : drow0;
+                    Cycle<CF, 0, true>::run(pm, src, flip, lg, crow, s0, T, true, first, p.one,
+                                            p.neg_one);
+                    first = nfirst;
+                    transform(tsn, j, punct_tag);
+                }
+            };
+            if (p.P == 1) cycles(std::false_type{});
+            else cycles(std::true_type{});
         }
         if (ncyc * V < nst)   // (the last chunk of an edge block)
             Cycle<CF, 0, false>::run(pm, src, flip, lg, drow + size_t(ncyc * V) * ROW, ncyc * V, nst, true,
