@@ -21,6 +21,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_
     -o ${o}_fused_C4 python tools/one_decode.py C4 2 0 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_kernel -s 1 -c 1 \
     -o ${o}_fused_c2_2p26 python tools/one_decode.py C2 2 0 1 67108864 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_kernel -s 1 -c 1 \
+    -o ${o}_fused_C3a python tools/one_decode.py C3a 2 0 1 > /dev/null 2>&1
 if [ -f paper_1608_00066_b200/build/variants/timing.so ]; then
   PBVD_TIMING_SAVE=${o}_timing_c2.npy PBVD_LIB=$PWD/paper_1608_00066_b200/build/variants/timing.so timeout 300 python tools/exp_timing.py C2 > ${o}_timing_c2.txt 2>&1
 fi
