@@ -139,22 +139,23 @@ def test_host_pipeline_matches_oracle(P, orc, n_streams):
         assert np.array_equal(host, want), (cname, pname, n_info)
 
 
-@pytest.mark.parametrize("fused,ws_mib", [(True, 4), (True, 1), (False, 4)])
-def test_small_workspace_matches_oracle(P, orc, fused, ws_mib):
+@pytest.mark.parametrize("fused,ws_mib,pname", [(True, 4, "1/2"), (True, 1, "1/2"), (True, 1, "3/4"),
+                                                 (False, 4, "1/2"), (False, 4, "2/3")])
+def test_small_workspace_matches_oracle(P, orc, fused, ws_mib, pname):
     """A survivor workspace smaller than the stream: the fused kernel runs ONE
     launch whose jobs recycle the workspace's regions (job gw -> region
     gw % regions once the region's previous job has traced back; 1 MiB = 6
     regions for 256 jobs), the two-kernel path runs many waves (interior-block
     groups, edges riding with the first / last).  Both are bit-exact against
     the oracle and against the one-wave decode."""
-    code = synth.CODES["k7"]
+    code, punct = synth.CODES["k7"], synth.PUNCT[pname]
     n_info = 1 << 22
-    info, llr = synth.make_stream(code, n_info, 3.0, 31)
-    want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, 512, 42))
+    info, llr = synth.make_stream(code, n_info, 3.0, 31, punct)
+    want = orc.pack_bits(orc.decode(code, llr.numpy(), n_info, 512, 42, punct=punct))
     d_llr = llr.cuda()
-    ref = P.Decoder(code["K"], code["polys"], 512, 42, fused=fused)
+    ref = P.Decoder(code["K"], code["polys"], 512, 42, punct=punct, fused=fused)
     one = ref.decode(d_llr, n_info).cpu().numpy()
-    dec = P.Decoder(code["K"], code["polys"], 512, 42, fused=fused)
+    dec = P.Decoder(code["K"], code["polys"], 512, 42, punct=punct, fused=fused)
     dec.set_workspace_limit(ws_mib << 20)
     dec.set_profiling(True)
     got = dec.decode(d_llr, n_info)
