@@ -37,11 +37,11 @@
 //     32*WPS contiguous words per stage, full 128-byte lines).
 //   * every warp is an autonomous pipeline (no CTA barrier anywhere): it
 //     copies its blocks' soft windows of the NEXT chunk with 16-byte cp.async
-//     (LDGSTS) while it computes the current one, then (depunctured if
-//     needed) interleaves them into per-(pair, stage) words of biased bytes
-//     u_r = lam_r + 128 for both blocks, read with one LDS per stage one stage
-//     ahead of use and zero-extended to 16x2 by PRMT.  Shared memory per warp
-//     is ~12 KB, so occupancy is set by registers, not shared memory.
+//     (LDGSTS) while it computes the current one, then (depunctured on the
+//     fly for punctured codes) interleaves them into per-(pair, stage) words
+//     of biased bytes u_r = lam_r + 128 for both blocks, read with one LDS per
+//     stage one stage ahead of use and zero-extended to 16x2 by PRMT.  Shared
+//     memory per warp is ~11 KB; the launch caps residency at 12 warps per SM.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -127,7 +127,7 @@ struct Cfg {
     static constexpr int LSTR = ((NG * G * LW + 31) / 32) * 32 + cmax(32 / PPW, LW);
     // per warp: raw windows [2][BPW][RAWB], operands [2][PPW][LSTR]
     static constexpr int NCYC = (T + V - 1) / V;          // cycles per chunk
-    // window slot of block i in raw[.] / dep[]: even blocks first, then odd
+    // window slot of block i in raw[.]: even blocks first, then odd
     // (h-major), so the PPW pairs' same-half windows are RAWB apart and a
     // warp's 32-bit transform reads hit 8 banks instead of 4 (a 16-byte
     // aligned window start can only reach banks = 0 mod 4)
