@@ -734,6 +734,9 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             __syncwarp();
         }
     }
+#ifdef PBVD_EXP_TIMING
+    if (p.dbg && lane == 0) p.dbg[32 * gw + 30] = gtime();   // prologue done
+#endif
     for (int c = 0; c < nchunks; ++c) {
         const int nst = min(T, span - c * T);
         const bool next = c + 1 < nchunks;
