@@ -441,7 +441,10 @@ __device__ __forceinline__ int64_t kept_before(const FwdParams& p, int64_t s, in
 // (streams larger than the workspace).  Separate instantiations, so the
 // default kernel carries none of that code (measured: the recycling code
 // alone costs the default kernel ~0.8 %, 8 more registers).
-template <class CF, bool FUSED, bool MIRROR = false, bool RECYCLE = MIRROR>
+// PUNCT: punctured codes (P > 1): the soft windows are depunctured inside the
+// transform slices; a separate instantiation so the dense kernels carry none
+// of that code (a run-time split of the cycle loop cost them 0.4-0.8 %).
+template <class CF, bool FUSED, bool MIRROR = false, bool RECYCLE = MIRROR, bool PUNCT = false>
 __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(const __grid_constant__ FwdParams p) {
     constexpr int V = CF::V, N = CF::N, S = CF::S, W = CF::W, R = CF::R, T = CF::T;
     constexpr int BPW = CF::BPW, PPW = CF::PPW, ROW = CF::ROW, RAWB = CF::RAWB;
@@ -457,6 +460,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
 
     // warp unit: interior warps first (BPW consecutive interior blocks), then
     // one unit per edge block (all lane groups replicate that block)
+    if (PUNCT != (p.P != 1)) __trap();         // the host picks the instantiation by P
     const int64_t gw = int64_t(blockIdx.x) * CF::NWARP + warp;
     const bool edge = gw >= p.n_int_warps;
     const int e = int(gw - p.n_int_warps);
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     // kept in shared memory, so a chunk's kept index needs 32-bit arithmetic
     // only (the per-chunk 64-bit divisions cost C3 2 %)
     constexpr int NBL_L = (BPW + 31) / 32;
-    if (p.P != 1) {
+    if constexpr (PUNCT) {
 #pragma unroll
         for (int m = 0; m < NBL_L; ++m) {
             const int i = lane + 32 * m;
@@ -508,11 +512,14 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
     // kept index (relative to the launch window) of stage s0 >= 0 of lane block i
     // (only lane i's own entries are read: no barrier needed)
     auto kept_at = [&](int i, int s0) -> int64_t {
-        if (p.P == 1) return (block_lo(i) + s0) * R - p.kb_ws0;
-        const unsigned u = unsigned(pr_s[i] + s0);
-        const unsigned q = u / unsigned(p.P);
-        const unsigned r = u - q * unsigned(p.P);
-        return (pq_s[i] + int64_t(q)) * p.kp + p.cum[r] - p.kb_ws0;
+        if constexpr (!PUNCT) {
+            return (block_lo(i) + s0) * R - p.kb_ws0;
+        } else {
+            const unsigned u = unsigned(pr_s[i] + s0);
+            const unsigned q = u / unsigned(p.P);
+            const unsigned r = u - q * unsigned(p.P);
+            return (pq_s[i] + int64_t(q)) * p.kp + p.cum[r] - p.kb_ws0;
+        }
     };
 
     // 16-byte cp.async of chunk c's soft windows: lane i copies block i's
@@ -584,7 +591,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
         for (int h = 0; h < 2; ++h) {
             const int i = edge ? 0 : 2 * tp + h;
             const int o0 = int(wo[i]);
-            if (p.P == 1) {
+            if constexpr (!PUNCT) {
                 ts.base[h] = rb + size_t(CF::wslot(i)) * RAWB + (o0 & ~3);
                 ts.sh[h] = uint32_t(o0 & 3) * 8u;
             } else {
@@ -722,8 +729,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             const TfmSetup ts0 = transform_setup(0);
 #pragma unroll 1
             for (int j = 0; j < CF::NCYC; ++j) {
-                if (p.P == 1) transform(ts0, j, std::false_type{});
-                else transform(ts0, j, std::true_type{});
+                transform(ts0, j, std::integral_constant<bool, PUNCT>{});
             }
         }
         __syncwarp();
@@ -771,7 +777,8 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
             // (within a cycle Cycle<> loads one stage ahead); the read past the
             // chunk's last stage stays inside the operand row's padding
             const TfmSetup tsn = transform_setup(c + 1);      // harmless past the last chunk
-            auto cycles = [&](auto punct_tag) {
+            {
+                const std::integral_constant<bool, PUNCT> punct_tag{};
                 XY<CF> first = src.load(0);
 #pragma unroll 1
                 for (int j = 0; j < ncyc; ++j) {
@@ -783,9 +790,7 @@ __global__ void __launch_bounds__(CF::NT) __maxnreg__(CF::MAXREG) fwd_kernel(con
                     first = nfirst;
                     transform(tsn, j, punct_tag);
                 }
-            };
-            if (p.P == 1) cycles(std::false_type{});
-            else cycles(std::true_type{});
+            }
         }
         if (ncyc * V < nst)   // (the last chunk of an edge block)
             Cycle<CF, 0, false>::run(pm, src, flip, lg, drow + size_t(ncyc * V) * ROW, ncyc * V, nst, true,

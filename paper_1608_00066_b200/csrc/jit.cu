@@ -219,11 +219,12 @@ void mkdirs(const std::string& d) {
         if (k == d.size() || d[k] == '/') mkdir(d.substr(0, k).c_str(), 0755);
 }
 
-// kernels per variant: fwd, fused, fused+mirror, traceback, fused+recycle
-constexpr int NKERN = 5;
+// kernels per variant: fwd, fused, fused+mirror, traceback, fused+recycle,
+// then the four forward kernels of punctured codes
+constexpr int NKERN = 9;
 
 // cache file: "PBVDJIT3\n" + NKERN lowered names (one per line) + cubin bytes
-constexpr char MAGIC[] = "PBVDJIT3\n";
+constexpr char MAGIC[] = "PBVDJIT4\n";
 
 bool cache_load(const std::string& path, std::string names[NKERN], std::string* cubin) {
     std::string all;
@@ -281,7 +282,11 @@ bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[N
                                       std::string("pbvd::fwd_kernel<") + cfg + ", true>",
                                       std::string("pbvd::fwd_kernel<") + cfg + ", true, true>",
                                       std::string("pbvd::tb_kernel<") + cfg + ">",
-                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, false, true>"};
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, false, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", false, false, false, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, false, false, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true, true, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, false, true, true>"};
     const std::string source = "// pbvd JIT: " + std::string(cfg) +
                                "\n#include \"fwd.cuh\"\n#include \"tb.cuh\"\n";
     const std::string sdir = src_dir();
@@ -385,6 +390,10 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
     ent->v.k_mirror = reinterpret_cast<const void*>(ks[2]);
     ent->v.k_tb = reinterpret_cast<const void*>(ks[3]);
     ent->v.k_recycle = reinterpret_cast<const void*>(ks[4]);
+    ent->v.k_fwd_p = reinterpret_cast<const void*>(ks[5]);
+    ent->v.k_fused_p = reinterpret_cast<const void*>(ks[6]);
+    ent->v.k_mirror_p = reinterpret_cast<const void*>(ks[7]);
+    ent->v.k_recycle_p = reinterpret_cast<const void*>(ks[8]);
     ent->v.prepared = 0;
     g_jit.push_back(std::move(ent));
     return &g_jit.back()->v;

@@ -139,10 +139,14 @@ int ensure_prepared(pbvd_t h, const Variant* v) {
     std::lock_guard<std::mutex> lk(g_prep_mu);
     const uint64_t bit = uint64_t(1) << (h->device & 63);
     if (!(v->prepared & bit)) {
-        const std::pair<const void*, size_t> ks[5] = {{v->k_fwd, fwd_smem(v->smem_fwd)},
+        const std::pair<const void*, size_t> ks[9] = {{v->k_fwd, fwd_smem(v->smem_fwd)},
                                                        {v->k_fused, fwd_smem(v->smem_fused)},
                                                        {v->k_mirror, fwd_smem(v->smem_fused)},
                                                        {v->k_recycle, fwd_smem(v->smem_fused)},
+                                                       {v->k_fwd_p, fwd_smem(v->smem_fwd)},
+                                                       {v->k_fused_p, fwd_smem(v->smem_fused)},
+                                                       {v->k_mirror_p, fwd_smem(v->smem_fused)},
+                                                       {v->k_recycle_p, fwd_smem(v->smem_fused)},
                                                        {v->k_tb, v->smem_tb}};
         for (const auto& k : ks) {
             cudaError_t e = cudaFuncSetAttribute(k.first, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -447,11 +451,13 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
             fp.dbg = dbg;
         }
 #endif
-        cudaError_t le = h->fused ? launch(fp.n_mirror > 0 ? v->k_mirror
-                                           : fp.n_regions > 0 ? v->k_recycle : v->k_fused, fgrid, v->NT,
-                                           fwd_smem(v->smem_fused), stream, fp, false)
-                                  : launch(v->k_fwd, fgrid, v->NT, fwd_smem(v->smem_fwd), stream, fp,
-                                           false);
+        const bool punct = h->P > 1;     // the PUNCT instantiations (depuncture in the transform)
+        const void* kf = fp.n_mirror > 0 ? (punct ? v->k_mirror_p : v->k_mirror)
+                         : fp.n_regions > 0 ? (punct ? v->k_recycle_p : v->k_recycle)
+                                            : (punct ? v->k_fused_p : v->k_fused);
+        cudaError_t le = h->fused ? launch(kf, fgrid, v->NT, fwd_smem(v->smem_fused), stream, fp, false)
+                                  : launch(punct ? v->k_fwd_p : v->k_fwd, fgrid, v->NT,
+                                           fwd_smem(v->smem_fwd), stream, fp, false);
         if (le != cudaSuccess) return cuda_fail(h, le, "forward kernel launch");
 #ifdef PBVD_EXP_TIMING
         if (dump) {

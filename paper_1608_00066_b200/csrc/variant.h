@@ -31,6 +31,11 @@ struct Variant {
     const void* k_fused;    // fwd_kernel<CF, true>(FwdParams)
     const void* k_mirror;   // fwd_kernel<CF, true, true>(FwdParams): fused + mirror copies (+ region recycling)
     const void* k_recycle;  // fwd_kernel<CF, true, false, true>(FwdParams): fused, recycled survivor regions
+    // the same four forward kernels for punctured codes (PUNCT = true)
+    const void* k_fwd_p;
+    const void* k_fused_p;
+    const void* k_mirror_p;
+    const void* k_recycle_p;
     const void* k_tb;       // tb_kernel<CF>(TbParams)
     mutable uint64_t prepared;   // per-device bit: dynamic smem attribute set
 };
