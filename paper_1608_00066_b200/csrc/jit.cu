@@ -220,11 +220,12 @@ void mkdirs(const std::string& d) {
 }
 
 // kernels per variant: fwd, fused, fused+mirror, traceback, fused+recycle,
-// then the four forward kernels of punctured codes
-constexpr int NKERN = 9;
+// then the four forward kernels of punctured codes, then mirror+recycle
+// (dense, punctured); the plain mirror kernels carry no recycling code
+constexpr int NKERN = 11;
 
 // cache file: "PBVDJIT3\n" + NKERN lowered names (one per line) + cubin bytes
-constexpr char MAGIC[] = "PBVDJIT4\n";
+constexpr char MAGIC[] = "PBVDJIT5\n";
 
 bool cache_load(const std::string& path, std::string names[NKERN], std::string* cubin) {
     std::string all;
@@ -280,13 +281,15 @@ bool jit_compile(int K, int R, const uint32_t* polys, int W, std::string names[N
                   polys[0], polys[1], R > 2 ? polys[2] : 0u, R > 3 ? polys[3] : 0u, W);
     const std::string exprs[NKERN] = {std::string("pbvd::fwd_kernel<") + cfg + ", false>",
                                       std::string("pbvd::fwd_kernel<") + cfg + ", true>",
-                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true, false>",
                                       std::string("pbvd::tb_kernel<") + cfg + ">",
                                       std::string("pbvd::fwd_kernel<") + cfg + ", true, false, true>",
                                       std::string("pbvd::fwd_kernel<") + cfg + ", false, false, false, true>",
                                       std::string("pbvd::fwd_kernel<") + cfg + ", true, false, false, true>",
-                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true, true, true>",
-                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, false, true, true>"};
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true, false, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, false, true, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true, true>",
+                                      std::string("pbvd::fwd_kernel<") + cfg + ", true, true, true, true>"};
     const std::string source = "// pbvd JIT: " + std::string(cfg) +
                                "\n#include \"fwd.cuh\"\n#include \"tb.cuh\"\n";
     const std::string sdir = src_dir();
@@ -394,6 +397,8 @@ const Variant* jit_variant(int K, int R, const uint32_t* polys, int W, std::stri
     ent->v.k_fused_p = reinterpret_cast<const void*>(ks[6]);
     ent->v.k_mirror_p = reinterpret_cast<const void*>(ks[7]);
     ent->v.k_recycle_p = reinterpret_cast<const void*>(ks[8]);
+    ent->v.k_mirror_r = reinterpret_cast<const void*>(ks[9]);
+    ent->v.k_mirror_r_p = reinterpret_cast<const void*>(ks[10]);
     ent->v.prepared = 0;
     g_jit.push_back(std::move(ent));
     return &g_jit.back()->v;

@@ -38,6 +38,7 @@ void fill_shape(Variant& v) {
     v.jit = false;
     v.k_fwd = v.k_fused = v.k_mirror = v.k_recycle = v.k_tb = nullptr;
     v.k_fwd_p = v.k_fused_p = v.k_mirror_p = v.k_recycle_p = nullptr;
+    v.k_mirror_r = v.k_mirror_r_p = nullptr;
     v.prepared = 0;
 }
 
@@ -49,11 +50,13 @@ Variant make_variant(int rank) {
     v.default_rank = rank;
     v.k_fwd = reinterpret_cast<const void*>(&fwd_kernel<CF, false>);
     v.k_fused = reinterpret_cast<const void*>(&fwd_kernel<CF, true>);
-    v.k_mirror = reinterpret_cast<const void*>(&fwd_kernel<CF, true, true>);
+    v.k_mirror = reinterpret_cast<const void*>(&fwd_kernel<CF, true, true, false>);
+    v.k_mirror_r = reinterpret_cast<const void*>(&fwd_kernel<CF, true, true, true>);
     v.k_recycle = reinterpret_cast<const void*>(&fwd_kernel<CF, true, false, true>);
     v.k_fwd_p = reinterpret_cast<const void*>(&fwd_kernel<CF, false, false, false, true>);
     v.k_fused_p = reinterpret_cast<const void*>(&fwd_kernel<CF, true, false, false, true>);
-    v.k_mirror_p = reinterpret_cast<const void*>(&fwd_kernel<CF, true, true, true, true>);
+    v.k_mirror_p = reinterpret_cast<const void*>(&fwd_kernel<CF, true, true, false, true>);
+    v.k_mirror_r_p = reinterpret_cast<const void*>(&fwd_kernel<CF, true, true, true, true>);
     v.k_recycle_p = reinterpret_cast<const void*>(&fwd_kernel<CF, true, false, true, true>);
     v.k_tb = reinterpret_cast<const void*>(&tb_kernel<CF>);
     return v;

@@ -139,7 +139,9 @@ int ensure_prepared(pbvd_t h, const Variant* v) {
     std::lock_guard<std::mutex> lk(g_prep_mu);
     const uint64_t bit = uint64_t(1) << (h->device & 63);
     if (!(v->prepared & bit)) {
-        const std::pair<const void*, size_t> ks[9] = {{v->k_fwd, fwd_smem(v->smem_fwd)},
+        const std::pair<const void*, size_t> ks[11] = {{v->k_fwd, fwd_smem(v->smem_fwd)},
+                                                       {v->k_mirror_r, fwd_smem(v->smem_fused)},
+                                                       {v->k_mirror_r_p, fwd_smem(v->smem_fused)},
                                                        {v->k_fused, fwd_smem(v->smem_fused)},
                                                        {v->k_mirror, fwd_smem(v->smem_fused)},
                                                        {v->k_recycle, fwd_smem(v->smem_fused)},
@@ -452,7 +454,8 @@ int run_blocks(pbvd_t h, Workspace& W, const int8_t* llr, int64_t ws0, int64_t n
         }
 #endif
         const bool punct = h->P > 1;     // the PUNCT instantiations (depuncture in the transform)
-        const void* kf = fp.n_mirror > 0 ? (punct ? v->k_mirror_p : v->k_mirror)
+        const void* kf = fp.n_mirror > 0 ? (fp.n_regions > 0 ? (punct ? v->k_mirror_r_p : v->k_mirror_r)
+                                                             : (punct ? v->k_mirror_p : v->k_mirror))
                          : fp.n_regions > 0 ? (punct ? v->k_recycle_p : v->k_recycle)
                                             : (punct ? v->k_fused_p : v->k_fused);
         cudaError_t le = h->fused ? launch(kf, fgrid, v->NT, fwd_smem(v->smem_fused), stream, fp, false)

@@ -29,12 +29,14 @@ struct Variant {
     // cudaFuncSetAttribute / cudaLaunchKernelExC
     const void* k_fwd;      // fwd_kernel<CF, false>(FwdParams)
     const void* k_fused;    // fwd_kernel<CF, true>(FwdParams)
-    const void* k_mirror;   // fwd_kernel<CF, true, true>(FwdParams): fused + mirror copies (+ region recycling)
+    const void* k_mirror;   // fwd_kernel<CF, true, true, false>(FwdParams): fused + mirror copies
+    const void* k_mirror_r; // fwd_kernel<CF, true, true, true>: mirror copies + recycled survivor regions
     const void* k_recycle;  // fwd_kernel<CF, true, false, true>(FwdParams): fused, recycled survivor regions
     // the same four forward kernels for punctured codes (PUNCT = true)
     const void* k_fwd_p;
     const void* k_fused_p;
     const void* k_mirror_p;
+    const void* k_mirror_r_p;
     const void* k_recycle_p;
     const void* k_tb;       // tb_kernel<CF>(TbParams)
     mutable uint64_t prepared;   // per-device bit: dynamic smem attribute set
